@@ -1,0 +1,166 @@
+/*
+ * tvprox.h -- C ABI of libtvprox.so, the B200-native (sm_100a) batched TV
+ * proximity operators of arXiv 2204.03643 ("Total Variation Optimization
+ * Layers for Computer Vision").  Citation keys: P:n = PAPER.md line n.
+ *
+ * Notation (reading O1/O2): input y, output
+ *     x = prox(y, lam) = argmin_x 1/2 ||x - y||^2 + sum_i lam_i |x_{i+1} - x_i|
+ * (Eq. 1), D the forward difference (D z)_i = z_{i+1} - z_i, dual
+ * u in R^{n-1} with |u_i| <= lam_i (Eq. 5) and x = y - D^T u.
+ *
+ * Conventions shared by every call
+ *  - All data pointers are DEVICE pointers owned by the caller; the library
+ *    never allocates, frees or synchronises.  Every call is asynchronous on
+ *    `stream` (a cudaStream_t; NULL = legacy default stream).
+ *  - dtype selects fp32 or fp64 for I/O and arithmetic.
+ *  - Host-detectable argument errors return TVP_EINVAL before any launch;
+ *    a launch/driver failure returns TVP_ECUDA (message: tvp_last_error()).
+ *    Per-row conditions (non-convergence, non-finite input) never fail a
+ *    call; they are reported through row_iters.
+ *  - Outputs are bitwise deterministic run to run (no float atomics; all
+ *    reductions are fixed-order).
+ *  - In-place operation (x == y, Y == X, grad_y == grad_x) is allowed.
+ *  - Lines (1D rows, 2D rows and columns) may have 1 <= n <= tvp_max_line().
+ */
+#ifndef TVPROX_H_
+#define TVPROX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *tvp_stream_t;   /* == cudaStream_t */
+
+typedef enum { TVP_F32 = 0, TVP_F64 = 1 } tvp_dtype_t;
+
+typedef enum {
+    TVP_LAM_SCALAR = 0,      /* 1D + 2D: the by-value lam_scalar                      */
+    TVP_LAM_PER_ROW = 1,     /* 1D: device T[batch]                                    */
+    TVP_LAM_PER_EDGE = 2,    /* 1D: device T[batch][stride], entries 0..n-2 of a row   */
+    TVP_LAM_PER_CHANNEL = 3, /* 2D: device T[C] (the TV layer's lambda_c)   */
+    TVP_LAM_PER_PLANE = 4    /* 2D: device T[N*C]                                      */
+} tvp_lam_mode_t;
+
+typedef enum { TVP_OK = 0, TVP_EINVAL = 1, TVP_EUNSUPPORTED = 2, TVP_ECUDA = 3 } tvp_status_t;
+
+/* row_iters codes written by the forward calls */
+#define TVP_ITERS_NOT_CONVERGED (-1)   /* max iterations hit; x = y - D^T u (feasible dual) */
+#define TVP_ITERS_NONFINITE     (-2)   /* NaN/Inf in the row (or its lam): row set to NaN  */
+#define TVP_ITERS_STALL_FLAG    (1 << 16) /* or-ed into a count: accepted at a rounding-level fixed point */
+
+/* Longest line (1D row length n, 2D W and H) the register-resident solver takes. */
+int64_t tvp_max_line(tvp_dtype_t dt);
+
+/* ------------------------------------------------------------------ 1D --- */
+/*
+ * Saved-for-backward mask: 2 bits per edge, edge e (between samples e and
+ * e+1) of row b at bits 2*(e%16) of word b*tv1d_mask_words(n) + e/16.
+ * Codes: 0 fused (same segment), 1 jump up, 2 jump down, 3 segment boundary
+ * with zero jump (only where lam_e = 0; reading O23).  Padding bits are 0.
+ * The mask is the support S-bar of D x and its signs.
+ */
+size_t tv1d_mask_words(int64_t n);                 /* ceil((n-1)/16), 0 if n <= 1 */
+
+/*
+ * tv1d_prox_fwd -- batched 1D TV prox (Eq. 1), one problem per row,
+ * solved by projected Newton on the dual Eq. 5 with the free-set Newton system
+ * Eq. 6 and a projected quadratic-interpolation backtracking line
+ * search; duality-gap (KKT) stop test.
+ *   y, x        [batch][stride] rows, first n entries used (stride >= n).
+ *   lam         TVP_LAM_SCALAR: NULL, value in lam_scalar; PER_ROW: T[batch];
+ *               PER_EDGE: T[batch][stride] (entry e = weight of edge e, e < n-1).
+ *               lam >= 0; lam = 0 gives x = y bitwise.
+ *   mask        nullable; batch*tv1d_mask_words(n) uint32 (needed by the bwd).
+ *   row_iters   nullable; int32[batch]: PN iterations, or the TVP_ITERS_ codes.
+ * Errors: TVP_EINVAL if y/x NULL (batch > 0), n < 1, batch < 0, stride < n,
+ * lam_scalar < 0 or non-finite (SCALAR), lam NULL (other modes), or a 2D
+ * mode; TVP_EUNSUPPORTED if n > tvp_max_line(dt).
+ */
+tvp_status_t tv1d_prox_fwd(tvp_dtype_t dt, const void *y, void *x,
+                           int64_t batch, int64_t n, int64_t stride,
+                           const void *lam, tvp_lam_mode_t lm, double lam_scalar,
+                           uint32_t *mask, int32_t *row_iters, tvp_stream_t stream);
+
+/* Workspace of tv1d_prox_bwd in bytes (nonzero only for TVP_LAM_SCALAR). */
+size_t tv1d_bwd_workspace_bytes(tvp_dtype_t dt, int64_t batch, tvp_lam_mode_t lm);
+
+/*
+ * tv1d_prox_bwd -- vector-Jacobian product of tv1d_prox_fwd (Eq. 7-8,
+ * P:190-200, reading O12): grad_y = segment-wise mean of grad_x over the
+ * segments of the forward's mask; grad_lam from the same segments: a segment
+ * [a,b) with boundary signs s_L (edge a-1, 0 at the start) and s_R (edge b-1,
+ * 0 at the end) has dx/dlam = (s_R - s_L)/(b-a).
+ *   grad_x, grad_y  [batch][stride].
+ *   mask            from tv1d_prox_fwd of the same (batch, n).
+ *   grad_lam        nullable; SCALAR: T[1] (sum over rows); PER_ROW: T[batch];
+ *                   PER_EDGE: T[batch][stride] (e < n-1 written: s_e*(mean_L-mean_R)).
+ *   workspace       tv1d_bwd_workspace_bytes(...) bytes (may be NULL if 0).
+ */
+tvp_status_t tv1d_prox_bwd(tvp_dtype_t dt, const void *grad_x, const uint32_t *mask,
+                           void *grad_y, void *grad_lam,
+                           int64_t batch, int64_t n, int64_t stride, tvp_lam_mode_t lm,
+                           void *workspace, tvp_stream_t stream);
+
+/* ------------------------------------------------------------------ 2D --- */
+/*
+ * 2D anisotropic TV prox of Eq. 2 per plane of an NCHW tensor,
+ * computed as the paper does by `iters` = K iterations of Proximal Dykstra
+ * (Algorithm 1; "three or four iterations"), each iteration a
+ * row pass then a column pass of the 1D solver above.  One lam is shared by the
+ * rows and columns of a plane (reading O4).
+ *
+ * saved (training), uint32, same 2-bit codes as tv1d: the K row-mask sets
+ * [K][N*C][H][ceil((W-1)/16)] (set k-1 = row pass k, line = image row),
+ * followed by the K column-mask sets [K][N*C][W][ceil((H-1)/16)] (line = image
+ * column, column-major per plane).  Pass k >= 2 of each orientation
+ * warm-starts its projected Newton from the mask of pass k-1 (DESIGN.md a-11).
+ */
+size_t tv2d_saved_bytes(int64_t N, int64_t C, int64_t H, int64_t W, int iters);
+
+/* Workspace (bytes) for tv2d_prox_fwd / tv2d_prox_bwd with these sizes. */
+size_t tv2d_workspace_bytes(tvp_dtype_t dt, int64_t N, int64_t C, int64_t H, int64_t W, int iters);
+
+/*
+ * tv2d_prox_fwd -- X, Y: contiguous NCHW.  lam per TVP_LAM_SCALAR (lam_scalar),
+ * TVP_LAM_PER_CHANNEL (T[C]) or TVP_LAM_PER_PLANE (T[N*C]); lam >= 0.
+ * saved nullable (inference).  workspace: tv2d_workspace_bytes(...) bytes.
+ * line_iters nullable: int32 [K][2], max PN iterations over the lines of each
+ * pass (row, column); a value >= 2^20 means some line of that pass did not
+ * converge (diagnostics; written with integer atomics, deterministic).
+ * Errors: TVP_EINVAL for NULL X/Y/workspace, N,C < 0, H,W < 1, iters < 1,
+ * invalid lam; TVP_EUNSUPPORTED if H or W > tvp_max_line(dt).
+ */
+tvp_status_t tv2d_prox_fwd(tvp_dtype_t dt, const void *X, void *Y,
+                           int64_t N, int64_t C, int64_t H, int64_t W,
+                           const void *lam, tvp_lam_mode_t lm, double lam_scalar, int iters,
+                           void *saved, void *workspace, int32_t *line_iters,
+                           tvp_stream_t stream);
+
+/*
+ * tv2d_prox_bwd -- reverse mode through the K unrolled iterations of
+ * Algorithm 1, using the masks in `saved` from tv2d_prox_fwd.
+ *   grad_Y, grad_X  NCHW.
+ *   grad_lam        nullable; SCALAR: T[1]; PER_CHANNEL: T[C]; PER_PLANE: T[N*C].
+ *                   (per-process partial sums; a caller sharding N across GPUs
+ *                   all-reduces them).
+ */
+tvp_status_t tv2d_prox_bwd(tvp_dtype_t dt, const void *grad_Y, const void *saved,
+                           void *grad_X, void *grad_lam,
+                           int64_t N, int64_t C, int64_t H, int64_t W,
+                           tvp_lam_mode_t lm, int iters, void *workspace,
+                           tvp_stream_t stream);
+
+/* ------------------------------------------------------------ utilities --- */
+const char *tvp_status_string(tvp_status_t s);
+const char *tvp_last_error(void);          /* last TVP_ECUDA / TVP_EINVAL message (thread-local) */
+int tvp_version(void);                     /* 100 * major + minor */
+/* Number of kernel launches issued by this thread since the last reset. */
+int64_t tvp_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TVPROX_H_ */

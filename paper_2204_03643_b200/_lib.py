@@ -1,0 +1,82 @@
+"""ctypes loader for libtvprox.so (the C ABI in include/tvprox.h).
+
+Argument marshalling only.  The product path has no fallback: if the shared
+library is missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libtvprox.so")
+
+TVP_F32, TVP_F64 = 0, 1
+LAM_SCALAR, LAM_PER_ROW, LAM_PER_EDGE, LAM_PER_CHANNEL, LAM_PER_PLANE = 0, 1, 2, 3, 4
+TVP_OK, TVP_EINVAL, TVP_EUNSUPPORTED, TVP_ECUDA = 0, 1, 2, 3
+ITERS_NOT_CONVERGED, ITERS_NONFINITE, ITERS_STALL_FLAG = -1, -2, 1 << 16
+
+# every symbol include/tvprox.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "tvp_max_line", "tv1d_mask_words", "tv1d_prox_fwd", "tv1d_bwd_workspace_bytes", "tv1d_prox_bwd",
+    "tv2d_saved_bytes", "tv2d_workspace_bytes", "tv2d_prox_fwd", "tv2d_prox_bwd",
+    "tvp_status_string", "tvp_last_error", "tvp_version", "tvp_launch_count",
+]
+
+_lock = threading.Lock()
+_lib = None
+
+
+class TVProxError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load and type the library (once)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise TVProxError(
+                "libtvprox.so not found at %s: build it with `python -m paper_2204_03643_b200.build` "
+                "(there is no CPU fallback)" % path)
+        lib = ctypes.CDLL(path)
+        i64, i32, u64 = ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+        vp, dbl = ctypes.c_void_p, ctypes.c_double
+        lib.tvp_max_line.argtypes = [i32]
+        lib.tvp_max_line.restype = i64
+        lib.tv1d_mask_words.argtypes = [i64]
+        lib.tv1d_mask_words.restype = u64
+        lib.tv1d_prox_fwd.argtypes = [i32, vp, vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp]
+        lib.tv1d_prox_fwd.restype = i32
+        lib.tv1d_bwd_workspace_bytes.argtypes = [i32, i64, i32]
+        lib.tv1d_bwd_workspace_bytes.restype = u64
+        lib.tv1d_prox_bwd.argtypes = [i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, vp]
+        lib.tv1d_prox_bwd.restype = i32
+        lib.tv2d_saved_bytes.argtypes = [i64, i64, i64, i64, i32]
+        lib.tv2d_saved_bytes.restype = u64
+        lib.tv2d_workspace_bytes.argtypes = [i32, i64, i64, i64, i64, i32]
+        lib.tv2d_workspace_bytes.restype = u64
+        lib.tv2d_prox_fwd.argtypes = [i32, vp, vp, i64, i64, i64, i64, vp, i32, dbl, i32, vp, vp, vp, vp]
+        lib.tv2d_prox_fwd.restype = i32
+        lib.tv2d_prox_bwd.argtypes = [i32, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, vp, vp]
+        lib.tv2d_prox_bwd.restype = i32
+        lib.tvp_status_string.argtypes = [i32]
+        lib.tvp_status_string.restype = ctypes.c_char_p
+        lib.tvp_last_error.argtypes = []
+        lib.tvp_last_error.restype = ctypes.c_char_p
+        lib.tvp_version.argtypes = []
+        lib.tvp_version.restype = i32
+        lib.tvp_launch_count.argtypes = [i32]
+        lib.tvp_launch_count.restype = i64
+        _lib = lib
+        return lib
+
+
+def check(status: int, what: str):
+    if status != TVP_OK:
+        lib = load()
+        msg = lib.tvp_last_error().decode(errors="replace")
+        raise TVProxError("%s failed: %s (%s)" % (what, lib.tvp_status_string(status).decode(), msg))

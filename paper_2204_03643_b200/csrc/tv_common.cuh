@@ -1,0 +1,110 @@
+// tv_common.cuh -- shared device helpers of the sm_100a TV-prox kernels.
+//
+// Line layout used by every kernel: a "line" (1D row, 2D row or 2D column) of
+// n <= LPR*E samples is held by a group of LPR consecutive lanes of a warp;
+// lane l of the group holds the CONTIGUOUS samples i = l*E + k, k = 0..E-1,
+// in registers.  Edge i (between samples i and i+1) belongs to the lane that
+// holds sample i.  Edges i >= n-1 (and edges with lam_i = 0) are "pinned":
+// their dual is fixed at 0, which isolates the padding samples.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tvp {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <typename T> struct Num;
+template <> struct Num<float> {
+    static constexpr float eps = 5.9604645e-08f;   // 2^-24, unit roundoff
+    static constexpr int max_iters = 64;
+};
+template <> struct Num<double> {
+    static constexpr double eps = 1.1102230246251565e-16;  // 2^-53
+    static constexpr int max_iters = 100;
+};
+
+// Padded shared-memory index: one spare word every 32 so that lane l reading
+// sample l*E + k hits distinct banks (E a multiple of 32 or odd).
+__device__ __forceinline__ int spad(int i) { return i + (i >> 5); }
+__host__ __device__ constexpr int spad_len(int m) { return m + (m >> 5) + 1; }
+
+template <int W, typename T>
+__device__ __forceinline__ T shup(T v, int d) { return __shfl_up_sync(FULL, v, d, W); }
+template <int W, typename T>
+__device__ __forceinline__ T shdn(T v, int d) { return __shfl_down_sync(FULL, v, d, W); }
+template <int W, typename T>
+__device__ __forceinline__ T shxor(T v, int m) { return __shfl_xor_sync(FULL, v, m, W); }
+
+template <int W, typename T>
+__device__ __forceinline__ T group_sum(T v) {
+#pragma unroll
+    for (int m = W / 2; m >= 1; m >>= 1) v += shxor<W>(v, m);
+    return v;
+}
+template <int W, typename T>
+__device__ __forceinline__ T group_max(T v) {
+#pragma unroll
+    for (int m = W / 2; m >= 1; m >>= 1) v = max(v, shxor<W>(v, m));
+    return v;
+}
+
+// Group-wide vote: true iff pred holds on every lane of this lane's group.
+template <int W>
+__device__ __forceinline__ bool group_all(bool pred) {
+    unsigned b = __ballot_sync(FULL, !pred);
+    if (W == 32) return b == 0;
+    unsigned lane = threadIdx.x & 31;
+    unsigned gm = ((1u << W) - 1u) << (lane & ~(W - 1));
+    return (b & gm) == 0;
+}
+template <int W>
+__device__ __forceinline__ bool group_any(bool pred) { return !group_all<W>(!pred); }
+
+// Division by a small positive count.  fp32: MUFU reciprocal (<= 2 ulp).
+__device__ __forceinline__ float div_count(float a, int c) { return __fdividef(a, (float)c); }
+__device__ __forceinline__ double div_count(double a, int c) { return a / (double)c; }
+
+__device__ __forceinline__ float clampv(float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); }
+__device__ __forceinline__ double clampv(double v, double lo, double hi) { return fmin(fmax(v, lo), hi); }
+
+template <typename T> __device__ __forceinline__ bool finite_(T v) { return isfinite(v); }
+
+template <typename T> __device__ __forceinline__ T nan_();
+template <> __device__ __forceinline__ float nan_<float>() { return __int_as_float(0x7fc00000); }
+template <> __device__ __forceinline__ double nan_<double>() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+// 2-bit edge codes of the saved mask (include/tvprox.h).
+enum : uint32_t { CODE_FUSED = 0u, CODE_UP = 1u, CODE_DOWN = 2u, CODE_BOUNDARY = 3u };
+
+template <typename T>
+__device__ __forceinline__ uint32_t edge_code(T xl, T xr, bool lam_zero) {
+    return xr > xl ? CODE_UP : (xr < xl ? CODE_DOWN : (lam_zero ? CODE_BOUNDARY : CODE_FUSED));
+}
+
+// Extract the 2E-bit window of mask codes for edges [e0, e0+E) of one line
+// (word array `mw`, nw words).  Returns per-edge bitmasks: bnd = code != 0,
+// neg = code == DOWN, pos = code == UP.
+template <int E>
+__device__ __forceinline__ void mask_window(const uint32_t* __restrict__ mw, int nw, int e0,
+                                            uint32_t& bnd, uint32_t& pos, uint32_t& neg) {
+    bnd = pos = neg = 0;
+    int w0 = e0 >> 4;
+    int sh = (e0 & 15) * 2;
+    constexpr int NS = (2 * E + 31) / 32;   // words of the aligned window
+    uint32_t words[NS + 1];
+#pragma unroll
+    for (int j = 0; j <= NS; ++j) words[j] = (w0 + j < nw) ? __ldg(mw + w0 + j) : 0u;
+    uint32_t s[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) s[j] = __funnelshift_r(words[j], words[j + 1], sh);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        uint32_t c = (s[(2 * k) >> 5] >> ((2 * k) & 31)) & 3u;
+        bnd |= (c != 0u ? 1u : 0u) << k;
+        pos |= (c == CODE_UP ? 1u : 0u) << k;
+        neg |= (c == CODE_DOWN ? 1u : 0u) << k;
+    }
+}
+
+}  // namespace tvp

@@ -1,0 +1,5 @@
+// fp64 instantiation unit of the TV-prox kernels (sm_100a).
+#include "tv_launch_impl.cuh"
+namespace tvp {
+TVP_INSTANTIATE(double)
+}

@@ -1,0 +1,38 @@
+// tv_launch.h -- host-side launch interface between the C ABI (tvprox_abi.cu)
+// and the per-dtype kernel instantiation units (tv_f32.cu, tv_f64.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tvp {
+
+template <typename T> struct RowFwdArgs;
+template <typename T> struct ColFwdArgs;
+template <typename T> struct RowBwdArgs;
+template <typename T> struct ColBwdArgs;
+template <typename T> struct LamReduceArgs;
+
+// (E samples per lane, LPR lanes per line) chosen for a line length n.
+struct Geo { int E, LPR; };
+inline Geo pick_geo(int64_t n) {
+    if (n <= 16) return {2, 8};
+    if (n <= 32) return {4, 8};
+    if (n <= 56) return {7, 8};
+    if (n <= 64) return {8, 8};
+    if (n <= 128) return {4, 32};
+    if (n <= 224) return {7, 32};
+    if (n <= 256) return {8, 32};
+    if (n <= 512) return {16, 32};
+    return {32, 32};
+}
+constexpr int64_t kMaxLine = 1024;
+
+template <typename T> cudaError_t launch_row_fwd(const RowFwdArgs<T>& a, bool per_edge, bool dykstra, cudaStream_t s);
+template <typename T> cudaError_t launch_col_fwd(ColFwdArgs<T> a, cudaStream_t s);
+template <typename T> cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s);
+template <typename T> cudaError_t launch_col_bwd(ColBwdArgs<T> a, cudaStream_t s);
+template <typename T> cudaError_t launch_lam_reduce(const LamReduceArgs<T>& a, cudaStream_t s);
+
+void count_launch();
+
+}  // namespace tvp

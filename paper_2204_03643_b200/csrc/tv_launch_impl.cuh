@@ -1,0 +1,172 @@
+// tv_launch_impl.cuh -- launcher templates (included once per dtype unit).
+#pragma once
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+
+#include "tv_kernels.cuh"
+#include "tv_launch.h"
+
+namespace tvp {
+
+// Persistent grid: min(work, SMs x resident blocks per SM) for this kernel.
+template <typename K>
+static int persistent_grid(K kern, int threads, size_t smem, int64_t work_blocks) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> occ_cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int occ = 0;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto key = reinterpret_cast<const void*>(kern);
+        auto it = occ_cache.find(key);
+        if (it == occ_cache.end()) {
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+            occ_cache[key] = occ;
+        } else {
+            occ = it->second;
+        }
+    }
+    if (occ < 1) occ = 1;
+    int64_t g = std::min<int64_t>(work_blocks, (int64_t)sms * occ);
+    return (int)std::max<int64_t>(g, 1);
+}
+
+#define TVP_GEO_DISPATCH(n, ...)                                               \
+    do {                                                                       \
+        Geo g_ = pick_geo(n);                                                  \
+        if (g_.LPR == 8) {                                                     \
+            switch (g_.E) {                                                    \
+                case 2: { constexpr int E_ = 2, L_ = 8; __VA_ARGS__; } break;         \
+                case 4: { constexpr int E_ = 4, L_ = 8; __VA_ARGS__; } break;         \
+                case 7: { constexpr int E_ = 7, L_ = 8; __VA_ARGS__; } break;         \
+                default: { constexpr int E_ = 8, L_ = 8; __VA_ARGS__; } break;        \
+            }                                                                  \
+        } else {                                                               \
+            switch (g_.E) {                                                    \
+                case 4: { constexpr int E_ = 4, L_ = 32; __VA_ARGS__; } break;        \
+                case 7: { constexpr int E_ = 7, L_ = 32; __VA_ARGS__; } break;        \
+                case 8: { constexpr int E_ = 8, L_ = 32; __VA_ARGS__; } break;        \
+                case 16: { constexpr int E_ = 16, L_ = 32; __VA_ARGS__; } break;      \
+                default: { constexpr int E_ = 32, L_ = 32; __VA_ARGS__; } break;      \
+            }                                                                  \
+        }                                                                      \
+    } while (0)
+
+constexpr int kRowWPB = 4;
+constexpr int kColWPB = 8;
+
+template <typename T, int E, int LPR, bool PE, bool DYK>
+static cudaError_t row_fwd_t(const RowFwdArgs<T>& a, cudaStream_t s) {
+    constexpr int G = 32 / LPR;
+    constexpr int LP = line_pitch<E, LPR>();
+    const size_t smem = (size_t)kRowWPB * (DYK ? 2 : 1) * G * LP * sizeof(T);
+    auto kern = k_row_fwd<T, E, LPR, PE, DYK, kRowWPB>;
+    const int64_t groups = (a.nlines + G - 1) / G;
+    const int grid = persistent_grid(kern, kRowWPB * 32, smem, (groups + kRowWPB - 1) / kRowWPB);
+    kern<<<grid, kRowWPB * 32, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_row_fwd(const RowFwdArgs<T>& a, bool per_edge, bool dykstra, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    TVP_GEO_DISPATCH(a.n, {
+        if (dykstra) e = row_fwd_t<T, E_, L_, false, true>(a, s);
+        else if (per_edge) e = row_fwd_t<T, E_, L_, true, false>(a, s);
+        else e = row_fwd_t<T, E_, L_, false, false>(a, s);
+    });
+    return e;
+}
+
+template <int LPR> constexpr int col_tile() { return kColWPB * (32 / LPR) * (LPR == 32 ? 2 : 1); }
+
+template <typename T, int E, int LPR>
+static cudaError_t col_fwd_t(ColFwdArgs<T> a, cudaStream_t s) {
+    constexpr int LP = line_pitch<E, LPR>();
+    constexpr int TC = col_tile<LPR>();
+    a.TC = TC;
+    const size_t smem = (size_t)2 * TC * LP * sizeof(T);
+    auto kern = k_col_fwd<T, E, LPR, kColWPB>;
+    const int64_t tiles = a.planes * ((a.W + TC - 1) / TC);
+    const int grid = persistent_grid(kern, kColWPB * 32, smem, tiles);
+    kern<<<grid, kColWPB * 32, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_col_fwd(ColFwdArgs<T> a, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    TVP_GEO_DISPATCH(a.H, { e = col_fwd_t<T, E_, L_>(a, s); });
+    return e;
+}
+
+template <typename T, int E, int LPR, bool DYK, bool PE>
+static cudaError_t row_bwd_t(const RowBwdArgs<T>& a, cudaStream_t s) {
+    constexpr int G = 32 / LPR;
+    constexpr int LP = line_pitch<E, LPR>();
+    const size_t smem = (size_t)kRowWPB * (DYK ? 2 : 1) * G * LP * sizeof(T);
+    auto kern = k_row_bwd<T, E, LPR, DYK, PE, kRowWPB>;
+    const int64_t groups = (a.nlines + G - 1) / G;
+    const int grid = persistent_grid(kern, kRowWPB * 32, smem, (groups + kRowWPB - 1) / kRowWPB);
+    kern<<<grid, kRowWPB * 32, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    TVP_GEO_DISPATCH(a.n, {
+        if (dykstra) e = row_bwd_t<T, E_, L_, true, false>(a, s);
+        else if (per_edge) e = row_bwd_t<T, E_, L_, false, true>(a, s);
+        else e = row_bwd_t<T, E_, L_, false, false>(a, s);
+    });
+    return e;
+}
+
+template <typename T, int E, int LPR>
+static cudaError_t col_bwd_t(ColBwdArgs<T> a, cudaStream_t s) {
+    constexpr int LP = line_pitch<E, LPR>();
+    constexpr int TC = col_tile<LPR>();
+    a.TC = TC;
+    const size_t smem = (size_t)2 * TC * LP * sizeof(T);
+    auto kern = k_col_bwd<T, E, LPR, kColWPB>;
+    const int64_t tiles = a.planes * ((a.W + TC - 1) / TC);
+    const int grid = persistent_grid(kern, kColWPB * 32, smem, tiles);
+    kern<<<grid, kColWPB * 32, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_col_bwd(ColBwdArgs<T> a, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    TVP_GEO_DISPATCH(a.H, { e = col_bwd_t<T, E_, L_>(a, s); });
+    return e;
+}
+
+template <typename T>
+cudaError_t launch_lam_reduce(const LamReduceArgs<T>& a, cudaStream_t s) {
+    if (a.nout <= 0) return cudaSuccess;
+    int grid = (int)std::min<int64_t>(a.nout, 4096);
+    k_lam_reduce<T><<<grid, 256, 0, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+#define TVP_INSTANTIATE(T)                                                                         \
+    template cudaError_t launch_row_fwd<T>(const RowFwdArgs<T>&, bool, bool, cudaStream_t);        \
+    template cudaError_t launch_col_fwd<T>(ColFwdArgs<T>, cudaStream_t);                           \
+    template cudaError_t launch_row_bwd<T>(const RowBwdArgs<T>&, bool, bool, cudaStream_t);        \
+    template cudaError_t launch_col_bwd<T>(ColBwdArgs<T>, cudaStream_t);                           \
+    template cudaError_t launch_lam_reduce<T>(const LamReduceArgs<T>&, cudaStream_t);
+
+}  // namespace tvp
