@@ -146,7 +146,8 @@ def bwd1d_batch(brk, sgn, g, per_edge=False, nthreads=1):
     b, n = g.shape
     gy = np.empty_like(g)
     gl = np.zeros((b, max(n - 1, 0))) if per_edge else np.zeros(b)
-    _get().tvref_bwd1d_batch(b, n, _p(_i8(brk)), _p(_i8(sgn)), _p(g), _p(gy), _p(gl),
+    brk, sgn = _i8(brk), _i8(sgn)      # keep the converted copies alive across the call
+    _get().tvref_bwd1d_batch(b, n, _p(brk), _p(sgn), _p(g), _p(gy), _p(gl),
                              int(per_edge), int(nthreads))
     return gy, gl
 

@@ -11,13 +11,13 @@ def unpack_codes(mask_words, n):
     e = np.arange(max(n - 1, 0))
     if e.size == 0:
         return np.zeros((lines, 0), np.int8)
-    return ((m[:, e // 16] >> (2 * (e % 16)).astype(np.uint32)) & 3).astype(np.int8)
+    return np.ascontiguousarray(((m[:, e // 16] >> (2 * (e % 16)).astype(np.uint32)) & 3).astype(np.int8))
 
 
 def codes_to_brk_sgn(codes):
     codes = np.asarray(codes)
-    brk = (codes != 0).astype(np.int8)
-    sgn = np.where(codes == 1, 1, np.where(codes == 2, -1, 0)).astype(np.int8)
+    brk = np.ascontiguousarray((codes != 0).astype(np.int8))
+    sgn = np.ascontiguousarray(np.where(codes == 1, 1, np.where(codes == 2, -1, 0)).astype(np.int8))
     return brk, sgn
 
 
