@@ -61,6 +61,13 @@ __device__ __forceinline__ bool group_all(bool pred) {
 template <int W>
 __device__ __forceinline__ bool group_any(bool pred) { return !group_all<W>(!pred); }
 
+// Reciprocal of a small positive count.  fp32: MUFU.RCP (<= 1 ulp), fp64: IEEE.
+__device__ __forceinline__ float rcp_(float c) {
+    float r;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(c));
+    return r;
+}
+__device__ __forceinline__ double rcp_(double c) { return 1.0 / c; }
 // Division by a small positive count.  fp32: MUFU reciprocal (<= 2 ulp).
 __device__ __forceinline__ float div_count(float a, int c) { return __fdividef(a, (float)c); }
 __device__ __forceinline__ double div_count(double a, int c) { return a / (double)c; }

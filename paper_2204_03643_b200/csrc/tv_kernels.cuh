@@ -167,21 +167,30 @@ k_row_fwd(RowFwdArgs<T> a) {
     for (int64_t gi = (int64_t)blockIdx.x * WPB + warp; gi < ngroups; gi += (int64_t)gridDim.x * WPB) {
         const int64_t r0 = gi * G;
         // ---- a-1: coalesced load of G lines into the warp's staging buffer
+        {
+            constexpr int PER = (LPR * E + 31) / 32;
+            T v0[G][PER], v1[G][PER];
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-            const int64_t r = r0 + j;
-            T* b = bufA + j * LP;
-            const bool ok = r < a.nlines;
-            const T* s0 = a.src0 + r * a.stride;
-            const T* s1 = (DYK && a.src1) ? a.src1 + r * a.stride : nullptr;
-            for (int i = lane; i < LPR * E; i += 32) {
-                T v = T(0);
-                if (ok && i < n) {
-                    v = __ldg(s0 + i);
-                    if (DYK && s1) v += __ldg(s1 + i);
+            for (int j = 0; j < G; ++j) {
+                const int64_t r = r0 + j;
+                const bool ok = r < a.nlines;
+                const T* s0 = a.src0 + r * a.stride;
+                const T* s1 = (DYK && a.src1) ? a.src1 + r * a.stride : nullptr;
+#pragma unroll
+                for (int q = 0; q < PER; ++q) {
+                    const int i = q * 32 + lane;
+                    const bool in = ok && i < n;
+                    v0[j][q] = in ? __ldg(s0 + i) : T(0);
+                    v1[j][q] = (DYK && s1 && in) ? __ldg(s1 + i) : T(0);
                 }
-                b[spad(i)] = v;
             }
+#pragma unroll
+            for (int j = 0; j < G; ++j)
+#pragma unroll
+                for (int q = 0; q < PER; ++q) {
+                    const int i = q * 32 + lane;
+                    if (i < LPR * E) bufA[j * LP + spad(i)] = DYK ? v0[j][q] + v1[j][q] : v0[j][q];
+                }
         }
         __syncwarp();
         const int64_t r = r0 + grp;
@@ -276,14 +285,23 @@ k_col_fwd(ColFwdArgs<T> a) {
         const int tcw = min(TC, W - c0);
         const int64_t base = p * HW + c0;
         // ---- coalesced load of the [H x TC] tile, transposed into line-major smem
-        for (int idx = threadIdx.x; idx < H * TC; idx += nth) {
-            int h = idx / TC, c = idx - h * TC;
-            T v = T(0);
-            if (c < tcw) {
-                v = __ldg(a.Z + base + (int64_t)h * W + c);
-                if (a.Q) v += __ldg(a.Q + base + (int64_t)h * W + c);
+        constexpr int U = 8;
+        for (int i0 = threadIdx.x; i0 < H * TC; i0 += nth * U) {
+            T v0[U], v1[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int idx = i0 + q * nth;
+                const int h = idx / TC, c = idx - h * TC;
+                const bool in = idx < H * TC && c < tcw;
+                v0[q] = in ? __ldg(a.Z + base + (int64_t)h * W + c) : T(0);
+                v1[q] = (in && a.Q) ? __ldg(a.Q + base + (int64_t)h * W + c) : T(0);
             }
-            bufA[c * LP + spad(h)] = v;
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int idx = i0 + q * nth;
+                const int h = idx / TC, c = idx - h * TC;
+                if (idx < H * TC) bufA[c * LP + spad(h)] = v0[q] + v1[q];
+            }
         }
         for (int idx = threadIdx.x; idx < (LPR * E - H) * TC; idx += nth) {
             int h = H + idx / TC, c = idx % TC;
@@ -373,23 +391,36 @@ k_row_bwd(RowBwdArgs<T> a) {
     const int64_t ngroups = (a.nlines + G - 1) / G;
     for (int64_t gi = (int64_t)blockIdx.x * WPB + warp; gi < ngroups; gi += (int64_t)gridDim.x * WPB) {
         const int64_t r0 = gi * G;
+        {
+            constexpr int PER = (LPR * E + 31) / 32;
+            T v0[G][PER], v1[G][PER];
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-            const int64_t r = r0 + j;
-            const bool ok = r < a.nlines;
-            for (int i = lane; i < LPR * E; i += 32) {
-                T v = T(0), pb = T(0);
-                if (ok && i < n) {
+            for (int j = 0; j < G; ++j) {
+                const int64_t r = r0 + j;
+                const bool ok = r < a.nlines;
+#pragma unroll
+                for (int q = 0; q < PER; ++q) {
+                    const int i = q * 32 + lane;
+                    const bool in = ok && i < n;
                     if (DYK) {
-                        pb = a.A ? __ldg(a.A + r * a.stride + i) : T(0);
-                        v = __ldg(a.B + r * a.stride + i) - pb;
+                        v1[j][q] = (in && a.A) ? __ldg(a.A + r * a.stride + i) : T(0);
+                        v0[j][q] = in ? __ldg(a.B + r * a.stride + i) : T(0);
                     } else {
-                        v = __ldg(a.A + r * a.stride + i);
+                        v0[j][q] = in ? __ldg(a.A + r * a.stride + i) : T(0);
+                        v1[j][q] = T(0);
                     }
                 }
-                bufV[j * LP + spad(i)] = v;
-                if (DYK) bufP[j * LP + spad(i)] = pb;
             }
+#pragma unroll
+            for (int j = 0; j < G; ++j)
+#pragma unroll
+                for (int q = 0; q < PER; ++q) {
+                    const int i = q * 32 + lane;
+                    if (i < LPR * E) {
+                        bufV[j * LP + spad(i)] = DYK ? v0[j][q] - v1[j][q] : v0[j][q];
+                        if (DYK) bufP[j * LP + spad(i)] = v1[j][q];
+                    }
+                }
         }
         __syncwarp();
         const int64_t r = r0 + grp;
@@ -464,15 +495,26 @@ k_col_bwd(ColBwdArgs<T> a) {
         const int c0 = (int)(tile % tpp) * TC;
         const int tcw = min(TC, W - c0);
         const int64_t base = p * HW + c0;
-        for (int idx = threadIdx.x; idx < LPR * E * TC; idx += nth) {
-            int h = idx / TC, c = idx - h * TC;
-            T v = T(0), b = T(0);
-            if (c < tcw && h < H) {
-                b = a.B ? __ldg(a.B + base + (int64_t)h * W + c) : T(0);
-                v = __ldg(a.A + base + (int64_t)h * W + c) - b;
+        constexpr int U = 8;
+        for (int i0 = threadIdx.x; i0 < LPR * E * TC; i0 += nth * U) {
+            T va[U], vb[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int idx = i0 + q * nth;
+                const int h = idx / TC, c = idx - h * TC;
+                const bool in = idx < LPR * E * TC && c < tcw && h < H;
+                vb[q] = (in && a.B) ? __ldg(a.B + base + (int64_t)h * W + c) : T(0);
+                va[q] = in ? __ldg(a.A + base + (int64_t)h * W + c) : T(0);
             }
-            bufV[c * LP + spad(h)] = v;
-            bufB[c * LP + spad(h)] = b;
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int idx = i0 + q * nth;
+                const int h = idx / TC, c = idx - h * TC;
+                if (idx < LPR * E * TC) {
+                    bufV[c * LP + spad(h)] = va[q] - vb[q];
+                    bufB[c * LP + spad(h)] = vb[q];
+                }
+            }
         }
         __syncthreads();
         for (int cg = warp; cg < TC / G; cg += WPB) {

@@ -17,6 +17,11 @@
 // running sum uhat_i = u_{a-1} + sum_{j=a}^{i} (xhat_j - y_j), so d = uhat - u.
 // On a warp this is two segmented scans plus one reverse broadcast, entirely in
 // registers (no 3xN band storage, no Cholesky factor).
+//
+// One PN iteration is four fused lane passes over the E register-resident
+// samples (P1 bound set + segment numerators, P2 carry + division, P3 reverse
+// broadcast, P4 KKT test + uhat) and three warp scans; the Armijo line search
+// only runs when the full step would leave the box.
 #pragma once
 #include "tv_common.cuh"
 
@@ -33,339 +38,351 @@ struct Lam {
     __device__ __forceinline__ T at(int k) const { return PE ? e[PE ? k : 0] : r; }
 };
 
+template <int E> __device__ __forceinline__ bool bit(uint32_t m, int k) { return (m >> k) & 1u; }
+
+// Highest set bit of m below position k, or -1.
+__device__ __forceinline__ int prev_bit(uint32_t m, int k) {
+    uint32_t mm = k >= 32 ? m : (m & ((1u << k) - 1u));
+    return 31 - __clz(mm);
+}
+
 // ---------------------------------------------------------------------------
-// Eq. 6 partition solve: w <- xhat for bound set `bnd` (segments end at bound
-// edges; u holds the bound values +-lam on them, 0 on pinned edges).
+// Segmented exclusive scans over the LPR lanes of a line group.
+// fwd: carry of (a, c, f) with combine(L, R) = R.f ? R : (L.a + R.a, L.c + R.c, L.f);
+//      identity (0, 0, false).  c < 2^30.
 // ---------------------------------------------------------------------------
-template <typename T, int E, int LPR>
-__device__ __forceinline__ void pn_candidate(const T (&y)[E], const T (&u)[E], uint32_t bnd,
-                                             T (&w)[E], int l) {
-    // pass 1: lane aggregate of the segment left open at the lane's end
-    T s = T(0), ub = T(0);
-    int c = 0;
-    bool f = false;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-        s += y[k];
-        c += 1;
-        if ((bnd >> k) & 1u) { f = true; ub = u[k]; s = T(0); c = 0; }
-    }
-    // segmented inclusive scan over the group: (sum, count, left bound value)
+template <int LPR, typename T>
+__device__ __forceinline__ void seg_scan_fwd(T& a, int& c, bool f, int l) {
 #pragma unroll
     for (int d = 1; d < LPR; d <<= 1) {
-        T s2 = shup<LPR>(s, d);
-        T ub2 = shup<LPR>(ub, d);
+        T a2 = shup<LPR>(a, d);
         int cf2 = shup<LPR>(c | (f ? (1 << 30) : 0), d);
-        if (l >= d && !f) { s += s2; ub = ub2; c += cf2 & 0x3fffffff; f = (cf2 >> 30) & 1; }
-    }
-    T cs = shup<LPR>(s, 1), cub = shup<LPR>(ub, 1);
-    int cc = shup<LPR>(c, 1);
-    if (l == 0) { cs = T(0); cub = T(0); cc = 0; }
-    // pass 2: segment values at segment ends
-    s = cs; c = cc; ub = cub;
-    T first = T(0);
-    bool hf = false;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-        s += y[k];
-        c += 1;
-        if ((bnd >> k) & 1u) {
-            T v = div_count(s + u[k] - ub, c);
-            w[k] = v;
-            if (!hf) first = v;
-            hf = true;
-            ub = u[k]; s = T(0); c = 0;
+        if (l >= d && !f) {
+            a += a2;
+            c += cf2 & 0x3fffffff;
+            f = (cf2 >> 30) & 1;
         }
     }
-    // pass 3: reverse broadcast of each segment's value to its elements
-    T v = first;
-    bool fv = hf;
+    T ea = shup<LPR>(a, 1);
+    int ec = shup<LPR>(c, 1);
+    a = (l == 0) ? T(0) : ea;
+    c = (l == 0) ? 0 : (ec & 0x3fffffff);
+}
+
+// fwd with two summed values (a, b) and a flag.
+template <int LPR, typename T>
+__device__ __forceinline__ void seg_scan_fwd2(T& a, T& b, bool f, int l) {
+#pragma unroll
+    for (int d = 1; d < LPR; d <<= 1) {
+        T a2 = shup<LPR>(a, d), b2 = shup<LPR>(b, d);
+        int f2 = shup<LPR>((int)f, d);
+        if (l >= d && !f) { a += a2; b += b2; f = f2 != 0; }
+    }
+    T ea = shup<LPR>(a, 1), eb = shup<LPR>(b, 1);
+    a = (l == 0) ? T(0) : ea;
+    b = (l == 0) ? T(0) : eb;
+}
+
+// rev: value of the nearest flagged lane strictly to the right (0 if none).
+template <int LPR, typename T>
+__device__ __forceinline__ T seg_scan_rev(T v, bool f, int l) {
 #pragma unroll
     for (int d = 1; d < LPR; d <<= 1) {
         T v2 = shdn<LPR>(v, d);
-        int f2 = shdn<LPR>((int)fv, d);
-        if (l + d < LPR && !fv) { v = v2; fv = f2 != 0; }
+        int f2 = shdn<LPR>((int)f, d);
+        if (l + d < LPR && !f) { v = v2; f = f2 != 0; }
     }
-    T cur = shdn<LPR>(v, 1);
-#pragma unroll
-    for (int k = E - 1; k >= 0; --k) {
-        if ((bnd >> k) & 1u) cur = w[k]; else w[k] = cur;
-    }
+    T e = shdn<LPR>(v, 1);
+    return (l + 1 < LPR) ? e : T(0);
 }
+
+template <typename T> __device__ __forceinline__ T big_();
+template <> __device__ __forceinline__ float big_<float>() { return 3.0e38f; }
+template <> __device__ __forceinline__ double big_<double>() { return 1.0e300; }
 
 // ---------------------------------------------------------------------------
-// Duality-gap / KKT stop test of the candidate (w = xhat on entry) and Newton
-// direction (w = d on exit).  At the candidate the duality gap is
-// sum_{i in B} (lam_i |dx_i| - u_i dx_i), zero iff every bound edge's jump has
-// the sign of u_i, and the candidate is dual feasible iff |uhat_i| <= lam_i on
-// free edges (tested with a summation-error slack; bound edges are never
-// feasibility-tested, their uhat only echoes rounding -- DESIGN.md O8).
+// The solver.  y: centred samples (read-only); u: dual (in/out); w: output x
+// (centred).  pin: pinned edges.  warm_pos/warm_neg: edges that were up/down
+// jumps in a previous solve (warm start, DESIGN.md a-11).  lam_max: max lambda
+// of the line (slack bound).  Returns the line status: iterations (| 1<<16 if
+// accepted at a stall), or -1 (max iterations, w = x(u)).
 // ---------------------------------------------------------------------------
-template <typename T, int E, int LPR, bool PE>
-__device__ __forceinline__ bool pn_test_direction(const T (&y)[E], const T (&u)[E], uint32_t bnd,
-                                                  uint32_t pin, T (&w)[E], const Lam<T, E, PE>& lam,
-                                                  int l) {
-    T r = T(0), A = T(0);
-    bool f = false;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-        T t = w[k] - y[k];
-        r += t;
-        A += fabs(t);
-        if ((bnd >> k) & 1u) { r = u[k]; A = fabs(u[k]); f = true; }
-    }
-#pragma unroll
-    for (int d = 1; d < LPR; d <<= 1) {
-        T r2 = shup<LPR>(r, d), A2 = shup<LPR>(A, d);
-        int f2 = shup<LPR>((int)f, d);
-        if (l >= d && !f) { r += r2; A += A2; f = f2 != 0; }
-    }
-    T cr = shup<LPR>(r, 1), cA = shup<LPR>(A, 1);
-    if (l == 0) { cr = T(0); cA = T(0); }
-    T xnext = shdn<LPR>(w[0], 1);
-    constexpr T C = T(E + 2 * Log2<LPR>::v + 8);
-    const T eps = Num<T>::eps;
-    bool ok = true;
-    r = cr; A = cA;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-        T xk = w[k];
-        T xk1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
-        T t = xk - y[k];
-        r += t;
-        A += fabs(t);
-        if ((bnd >> k) & 1u) {
-            if (!((pin >> k) & 1u)) ok = ok && (u[k] * (xk1 - xk) >= T(0));
-            w[k] = T(0);
-            r = u[k];
-            A = fabs(u[k]);
-        } else {
-            T lk = lam.at(k);
-            ok = ok && (fabs(r) <= lk + eps * (T(2) * lk + C * A));
-            w[k] = r - u[k];
-        }
-    }
-    return group_all<LPR>(ok);
-}
-
-// Bound set at u: pinned edges plus edges at +-lam whose gradient g = D x(u)
-// points out of the box (exact comparison: u is clipped exactly to +-lam).
-template <typename T, int E, int LPR, bool PE>
-__device__ __forceinline__ uint32_t pn_bound_set(const T (&y)[E], const T (&u)[E], uint32_t pin,
-                                                 const Lam<T, E, PE>& lam, int l) {
-    T uprev = shup<LPR>(u[E - 1], 1);
-    if (l == 0) uprev = T(0);
-    T y0n = shdn<LPR>(y[0], 1), u0n = shdn<LPR>(u[0], 1);
-    T xk = y[0] + u[0] - uprev;
-    uint32_t b = pin;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-        T xk1 = (k + 1 < E) ? (y[(k + 1 < E) ? k + 1 : k] + u[(k + 1 < E) ? k + 1 : k] - u[k])
-                            : (y0n + u0n - u[k]);
-        T g = xk1 - xk;
-        T lk = lam.at(k);
-        bool out = (u[k] >= lk && g > T(0)) || (u[k] <= -lk && g < T(0));
-        b |= (out ? 1u : 0u) << k;
-        xk = xk1;
-    }
-    return b;
-}
-
-// Projected line search along u(alpha) = clip(u + alpha d):
-// Armijo  phi(u(alpha)) - phi(u) >= sigma g^T (u(alpha) - u), sigma = 1e-4,
-// with quadratic-interpolation backtracking safeguarded to [0.1, 0.5] alpha.
-// phi(u(alpha)) - phi(u) = -1/2 sum_j delta_j (2 x_j + delta_j), delta = x(u(alpha)) - x(u),
-// evaluated in this difference form for accuracy.  Applies the accepted step to u
-// on `run` groups.  Returns true iff the step changed u (group-uniform).
-template <typename T, int E, int LPR, bool PE>
-__device__ __forceinline__ bool pn_line_search(const T (&y)[E], T (&u)[E], const T (&d)[E],
-                                               uint32_t bnd, const Lam<T, E, PE>& lam, int l,
-                                               bool run) {
-    T uprev = shup<LPR>(u[E - 1], 1);
-    if (l == 0) uprev = T(0);
-    T y0n = shdn<LPR>(y[0], 1), u0n = shdn<LPR>(u[0], 1);
-    T slope = T(0);
-    {
-        T xk = y[0] + u[0] - uprev;
-#pragma unroll
-        for (int k = 0; k < E; ++k) {
-            T xk1 = (k + 1 < E) ? (y[(k + 1 < E) ? k + 1 : k] + u[(k + 1 < E) ? k + 1 : k] - u[k])
-                                : (y0n + u0n - u[k]);
-            slope = fma(xk1 - xk, d[k], slope);
-            xk = xk1;
-        }
-    }
-    slope = group_sum<LPR>(slope);
-    T alpha = T(1);
-    bool pending = run, accepted = false, changed = false;
-    for (int trial = 0; trial < 40; ++trial) {
-        if (!__any_sync(FULL, pending)) break;
-        T lk = lam.at(E - 1);
-        T dlast = ((bnd >> (E - 1)) & 1u) ? T(0) : clampv(u[E - 1] + alpha * d[E - 1], -lk, lk) - u[E - 1];
-        T duprev = shup<LPR>(dlast, 1);
-        if (l == 0) duprev = T(0);
-        T F = T(0), G = T(0);
-        bool ch = false;
-        T xk = y[0] + u[0] - uprev;
-#pragma unroll
-        for (int k = 0; k < E; ++k) {
-            T lk2 = lam.at(k);
-            T du = ((bnd >> k) & 1u) ? T(0) : clampv(u[k] + alpha * d[k], -lk2, lk2) - u[k];
-            T xk1 = (k + 1 < E) ? (y[(k + 1 < E) ? k + 1 : k] + u[(k + 1 < E) ? k + 1 : k] - u[k])
-                                : (y0n + u0n - u[k]);
-            T dl = du - duprev;
-            F = fma(dl, T(2) * xk + dl, F);
-            G = fma(xk1 - xk, du, G);
-            ch = ch || (du != T(0));
-            duprev = du;
-            xk = xk1;
-        }
-        F = group_sum<LPR>(F);
-        G = group_sum<LPR>(G);
-        ch = group_any<LPR>(ch);
-        if (pending) {
-            T gain = T(-0.5) * F;
-            if (gain >= T(1e-4) * G) {
-                pending = false; accepted = true; changed = ch;
-            } else {
-                T den = T(2) * (slope * alpha - gain);
-                T an = den > T(0) ? slope * alpha * alpha / den : T(0.5) * alpha;
-                alpha = clampv(an, T(0.1) * alpha, T(0.5) * alpha);
-                if (alpha < T(1e-12)) pending = false;
-            }
-        }
-    }
-    if (accepted && changed) {
-#pragma unroll
-        for (int k = 0; k < E; ++k) {
-            T lk = lam.at(k);
-            if (!((bnd >> k) & 1u)) u[k] = clampv(u[k] + alpha * d[k], -lk, lk);
-        }
-    }
-    return accepted && changed;
-}
-
-// Full solve of one line per group.  y: centred samples; u: dual (in/out);
-// w: output x (centred).  pin: pinned edges.  warm_pos/warm_neg: edges that
-// were up/down jumps in a previous solve (warm start, DESIGN.md a-11).
-// Returns the per-line status (iterations | stall flag, or -1).
 template <typename T, int E, int LPR, bool PE>
 __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], uint32_t pin,
                                         uint32_t warm_pos, uint32_t warm_neg,
                                         const Lam<T, E, PE>& lam, int l, bool active) {
     warm_pos &= ~pin;
     warm_neg &= ~pin;
+    T ymax = T(0), lmax = T(0);
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-        T lk = lam.at(k);
-        u[k] = ((warm_pos >> k) & 1u) ? lk : (((warm_neg >> k) & 1u) ? -lk : T(0));
+        const T lk = lam.at(k);
+        u[k] = bit<E>(warm_pos, k) ? lk : (bit<E>(warm_neg, k) ? -lk : T(0));
+        ymax = fmax(ymax, fabs(y[k]));
+        if (PE) lmax = fmax(lmax, lk);
     }
+    ymax = group_max<LPR>(ymax);
+    lmax = PE ? group_max<LPR>(lmax) : lam.r;
     uint32_t bnd = pin | warm_pos | warm_neg;
-    // iteration 0: candidate of the initial bound set; if not optimal, start from
-    // u = clip(uhat) (the clipped unconstrained maximiser when cold).
-    pn_candidate<T, E, LPR>(y, u, bnd, w, l);
-    bool ok = pn_test_direction<T, E, LPR, PE>(y, u, bnd, pin, w, lam, l);
-    bool run = active && !ok;
-    bool conv = active && ok, stall = false;
-    if (run) {
+    const T ynext = shdn<LPR>(y[0], 1);
+    const T eps = Num<T>::eps;
+    const T slackA = eps * T(E + 2 * Log2<LPR>::v + 8);   // summation-depth factor of the KKT slack
+    const T slack1 = T(1) + T(2) * eps;
+    const int maxit = Num<T>::max_iters;
+
+    bool run = active, first = true, fin = false, uchg = true;
+    bool conv = false, stall = false;
+    int it = 0;
+    for (int itw = 0;; ++itw) {
+        // ---------------- P1: bound set at u (Bertsekas rule: at a bound with the
+        // gradient g = D x(u) pointing out of the box) fused with the lane-local part
+        // of the Eq. 6 partition solve: each segment ending in the lane gets
+        //   xhat = (sum_y - u_{a-1} + u_{b-1}) / len ;  s carries sum_y - u_{a-1}.
+        const bool upd = run && !first && !fin;
+        const uint32_t keep = upd ? pin : bnd;
+        const T uprev0 = shup<LPR>(u[E - 1], 1);
+        const T uprev = (l == 0) ? T(0) : uprev0;
+        const T unext = shdn<LPR>(u[0], 1);
+        uint32_t nb = 0;
+        T s = T(0), cnt = T(0), numf = T(0);
+        bool hf = false;
+        T xk = y[0] + u[0] - uprev;
 #pragma unroll
         for (int k = 0; k < E; ++k) {
-            T lk = lam.at(k);
-            if (!((bnd >> k) & 1u)) u[k] = clampv(u[k] + w[k], -lk, lk);
+            const T thr = upd ? lam.at(k) : big_<T>();
+            const T xk1 = (k + 1 < E) ? (y[(k + 1 < E) ? k + 1 : k] + u[(k + 1 < E) ? k + 1 : k] - u[k])
+                                      : (ynext + unext - u[k]);
+            const T g = xk1 - xk;
+            xk = xk1;
+            const bool bk = bit<E>(keep, k) || ((fabs(u[k]) >= thr) && (u[k] * g > T(0)));
+            if (bk) nb |= 1u << k;
+            s += y[k];
+            cnt += T(1);
+            const T num = s + u[k];
+            const T val = num * rcp_(cnt);
+            numf = (bk && !hf) ? num : numf;
+            w[k] = bk ? (hf ? val : num) : w[k];
+            hf = hf || bk;
+            s = bk ? -u[k] : s;
+            cnt = bk ? T(0) : cnt;
         }
-    }
-    int it = 1;        // candidate evaluations of this group's line
-    int itw = 1;       // warp-uniform loop counter
-    const int maxit = Num<T>::max_iters;
-    while (itw < maxit && __any_sync(FULL, run)) {
-        ++itw;
-        uint32_t nb = pn_bound_set<T, E, LPR, PE>(y, u, pin, lam, l);
-        if (run) bnd = nb;
-        pn_candidate<T, E, LPR>(y, u, bnd, w, l);
-        bool ok2 = pn_test_direction<T, E, LPR, PE>(y, u, bnd, pin, w, lam, l);
-        if (run) it += 1;
-        if (run && ok2) { conv = true; run = false; }
-        bool ch = pn_line_search<T, E, LPR, PE>(y, u, w, bnd, lam, l, run);
-        if (run && !ch) { stall = true; run = false; }
-    }
-    // output: the candidate of the final (u, B) when converged/stalled, else x(u)
-    pn_candidate<T, E, LPR>(y, u, bnd, w, l);
-    T uprev = shup<LPR>(u[E - 1], 1);
-    if (l == 0) uprev = T(0);
-    if (run) {
+        const bool bchg = group_any<LPR>(nb != bnd);
+        if (upd && !uchg && !bchg) { stall = true; run = false; }
+        bnd = nb;
+        const int hb = 31 - __clz(bnd);              // -1 if none
+        const bool fl = bnd != 0u;
+        const T s_tail = s;                           // sum_y(tail) - u(last bound)
+        const int cnt_tail = E - 1 - hb;
+        T cs = s;
+        int cc = cnt_tail;
+        seg_scan_fwd<LPR>(cs, cc, fl, l);
+
+        // ---------------- P2/P3: the lane's first segment gets the carry; reverse
+        // broadcast of each segment's value to its samples.
+        const int fb = __ffs(bnd) - 1;                // -1 if none
+        const uint32_t firstm = (bnd & (0u - bnd)) * 2u - 1u;   // bits 0..fb
+        const T fv = (numf + cs) * rcp_(T(fb + 1 + cc));
+        T cur = seg_scan_rev<LPR>(fv, fl, l);
 #pragma unroll
-        for (int k = 0; k < E; ++k) w[k] = y[k] + u[k] - (k > 0 ? u[k > 0 ? k - 1 : 0] : uprev);
+        for (int k = E - 1; k >= 0; --k) {
+            T v = bit<E>(bnd, k) ? w[k] : cur;
+            v = bit<E>(firstm, k) ? fv : v;
+            w[k] = v;
+            cur = v;
+        }
+        if (fin) break;
+
+        // ---------------- P4: KKT / zero-duality-gap test of the candidate, uhat -> w.
+        // uhat_i = u_{a-1} + sum_{j=a..i} (xhat_j - y_j); free edges must satisfy
+        // |uhat_i| <= lam_i (up to a summation-error slack), bound edges must jump
+        // in the direction of u_i.
+        const T c_tail = w[E - 1];
+        T r = T(cnt_tail) * c_tail - s_tail;
+        T A = T(cnt_tail) * (fabs(c_tail) + ymax) + lmax;
+        seg_scan_fwd2<LPR>(r, A, fl, l);
+        const T xnext = shdn<LPR>(w[0], 1);
+        bool ok = true, clip = false, chg = false;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const T xh = w[k];
+            const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
+            const T t = xh - y[k];
+            r += t;
+            A += fabs(t);
+            const T lk = lam.at(k);
+            const bool bk = bit<E>(bnd, k);
+            const bool sgn_bad = (u[k] * (xh1 - xh) < T(0)) && !bit<E>(pin, k);
+            const T ar = fabs(r);
+            const bool infeas = ar > fma(slackA, A, lk * slack1);
+            ok = ok && !(bk ? sgn_bad : infeas);
+            clip = clip || (!bk && ar > lk);
+            chg = chg || (!bk && r != u[k]);
+            w[k] = bk ? u[k] : r;
+            A = bk ? fabs(u[k]) : A;
+            r = bk ? u[k] : r;
+        }
+        ok = group_all<LPR>(ok);
+        clip = group_any<LPR>(clip);
+        chg = group_any<LPR>(chg);
+        if (run) ++it;
+        if (run && ok) { conv = true; run = false; }
+
+        // ---------------- step: full Newton step when it stays in the box, else
+        // projected Armijo line search with quadratic-interpolation backtracking.
+        const bool fast = run && (first || !clip);
+        if (fast) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                const T lk = lam.at(k);
+                u[k] = bit<E>(bnd, k) ? u[k] : clampv(w[k], -lk, lk);
+            }
+            uchg = chg || first;
+        }
+        bool pending = run && !fast;
+        if (__any_sync(FULL, pending)) {
+            T alpha = T(1), slope = T(0);
+            bool accepted = false, lchg = false;
+            for (int trial = 0; trial < 30; ++trial) {
+                if (!__any_sync(FULL, pending)) break;
+                const T lkl = lam.at(E - 1);
+                const T dlast = bit<E>(bnd, E - 1) ? T(0)
+                                                   : clampv(u[E - 1] + alpha * (w[E - 1] - u[E - 1]), -lkl, lkl) - u[E - 1];
+                const T dp0 = shup<LPR>(dlast, 1);
+                T duprev = (l == 0) ? T(0) : dp0;
+                T F = T(0), G = T(0), S = T(0);
+                bool ch = false;
+                T x0 = y[0] + u[0] - uprev;
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    const T lk = lam.at(k);
+                    const T dk = bit<E>(bnd, k) ? T(0) : (w[k] - u[k]);
+                    const T du = clampv(u[k] + alpha * dk, -lk, lk) - u[k];
+                    const T x1 = (k + 1 < E) ? (y[(k + 1 < E) ? k + 1 : k] + u[(k + 1 < E) ? k + 1 : k] - u[k])
+                                             : (ynext + unext - u[k]);
+                    const T g = x1 - x0;
+                    const T dl = du - duprev;
+                    F = fma(dl, T(2) * x0 + dl, F);
+                    G = fma(g, du, G);
+                    S = fma(g, dk, S);
+                    ch = ch || (du != T(0));
+                    duprev = du;
+                    x0 = x1;
+                }
+                F = group_sum<LPR>(F);
+                G = group_sum<LPR>(G);
+                S = group_sum<LPR>(S);
+                ch = group_any<LPR>(ch);
+                if (trial == 0) slope = S;
+                if (pending) {
+                    const T gain = T(-0.5) * F;          // phi(u(alpha)) - phi(u)
+                    if (gain >= T(1e-4) * G) {
+                        pending = false; accepted = true; lchg = ch;
+                    } else {
+                        const T den = T(2) * (slope * alpha - gain);
+                        const T an = den > T(0) ? slope * alpha * alpha / den : T(0.5) * alpha;
+                        alpha = clampv(an, T(0.1) * alpha, T(0.5) * alpha);
+                        if (alpha < T(1e-12)) pending = false;
+                    }
+                }
+            }
+            if (run && !fast) {
+                if (accepted && lchg) {
+#pragma unroll
+                    for (int k = 0; k < E; ++k) {
+                        const T lk = lam.at(k);
+                        const T dk = bit<E>(bnd, k) ? T(0) : (w[k] - u[k]);
+                        u[k] = clampv(u[k] + alpha * dk, -lk, lk);
+                    }
+                    uchg = true;
+                } else {
+                    stall = true;                          // no ascent step exists at rounding level
+                    run = false;
+                }
+            }
+        }
+        first = false;
+        if (!__any_sync(FULL, run) || itw + 2 >= maxit) fin = true;
+    }
+    // lines still running hit max_iters: output the primal of the current dual
+    const T up0 = shup<LPR>(u[E - 1], 1);
+    if (run) {
+        const T upv = (l == 0) ? T(0) : up0;
+#pragma unroll
+        for (int k = 0; k < E; ++k) w[k] = y[k] + u[k] - (k > 0 ? u[k > 0 ? k - 1 : 0] : upv);
+        return -1;
     }
     if (conv) return it;
     if (stall) return it | (1 << 16);
-    return -1;
+    return 0;
 }
 
 // ---------------------------------------------------------------------------
 // Backward primitive: v <- segment-wise mean of v (Eq. 7 under reading O12:
 // the symmetric projector onto vectors constant on the segments).  Segments end
-// at edges in `bnd`; sgn(k) in {-1,0,+1} is the jump sign of edge k (pos/neg
-// bitmasks).  lam_part += sum over segments ending in this lane of
-// (s_R - s_L) * mean (dx/dlam = (s_R - s_L)/len).
+// at edges in `bnd`; the jump sign of edge k is +1 (pos), -1 (neg) or 0.
+// lam_part += sum over segments ending in this lane of (s_R - s_L) * mean
+// (dx/dlam = (s_R - s_L)/len).
 // ---------------------------------------------------------------------------
 template <typename T, int E, int LPR>
 __device__ __forceinline__ void seg_mean(T (&v)[E], uint32_t bnd, uint32_t pos, uint32_t neg, int l,
                                          T& lam_part) {
-    T s = T(0);
-    int c = 0;
-    int sl = 0;       // sign of the edge before the open segment
-    bool f = false;
+    // lane pass: lane-local segment sums at segment ends (the first segment of the
+    // lane still lacks the carry) and the open tail
+    T s = T(0), sf = T(0);
+    bool hf = false;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         s += v[k];
-        c += 1;
-        if ((bnd >> k) & 1u) {
-            f = true; s = T(0); c = 0;
-            sl = ((pos >> k) & 1u) ? 1 : (((neg >> k) & 1u) ? -1 : 0);
-        }
+        const bool bk = bit<E>(bnd, k);
+        sf = (bk && !hf) ? s : sf;
+        hf = hf || bk;
+        v[k] = bk ? s : v[k];
+        s = bk ? T(0) : s;
     }
+    const int hb = 31 - __clz(bnd);
+    const bool fl = bnd != 0u;
+    // carry: (tail sum, tail count) and the sign of the boundary before the tail
+    T cs = s;
+    int cc = E - 1 - hb;
+    seg_scan_fwd<LPR>(cs, cc, fl, l);
+    const int sl_own = hb < 0 ? 0 : (bit<E>(pos, hb & 31) ? 1 : (bit<E>(neg, hb & 31) ? -1 : 0));
+    // sign of the last boundary left of the lane (nearest flagged lane to the left)
+    int slc = sl_own;
+    bool fs = fl;
 #pragma unroll
     for (int d = 1; d < LPR; d <<= 1) {
-        T s2 = shup<LPR>(s, d);
-        int p2 = shup<LPR>(c | (f ? (1 << 30) : 0) | ((sl + 1) << 27), d);
-        if (l >= d && !f) {
-            s += s2; c += p2 & 0x7ffffff; f = (p2 >> 30) & 1; sl = ((p2 >> 27) & 3) - 1;
-        }
+        int s2 = shup<LPR>((slc + 2) | (fs ? 4 : 0), d);
+        if (l >= d && !fs) { slc = (s2 & 3) - 2; fs = (s2 & 4) != 0; }
     }
-    T cs = shup<LPR>(s, 1);
-    int cp = shup<LPR>(c | ((sl + 1) << 27), 1);
-    if (l == 0) { cs = T(0); cp = (1 << 27); }
-    s = cs; c = cp & 0x7ffffff; sl = ((cp >> 27) & 3) - 1;
-    T first = T(0);
-    bool hf = false;
+    int sle = shup<LPR>((slc + 2) | (fs ? 4 : 0), 1);
+    const int csl = (l == 0 || !(sle & 4)) ? 0 : ((sle & 3) - 2);
+    const int fb = __ffs(bnd) - 1;
+    const uint32_t firstm = (bnd & (0u - bnd)) * 2u - 1u;
+    const T fv = (sf + cs) * rcp_(T(fb + 1 + cc));
     T lp = T(0);
+    int prev_s = csl;
+    T cnt = T(0);
+    // means at segment ends and the lambda-gradient terms (s_R - s_L) * mean
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-        s += v[k];
-        c += 1;
-        if ((bnd >> k) & 1u) {
-            T m = div_count(s, c);
-            int sr = ((pos >> k) & 1u) ? 1 : (((neg >> k) & 1u) ? -1 : 0);
-            lp += T(sr - sl) * m;
-            v[k] = m;
-            if (!hf) first = m;
-            hf = true;
-            sl = sr; s = T(0); c = 0;
-        }
+        cnt += T(1);
+        const bool bk = bit<E>(bnd, k);
+        const bool isf = bit<E>(firstm, k);
+        const T m = isf ? fv : v[k] * rcp_(cnt);
+        const int sr = bit<E>(pos, k) ? 1 : (bit<E>(neg, k) ? -1 : 0);
+        lp += bk ? T(sr - prev_s) * m : T(0);
+        prev_s = bk ? sr : prev_s;
+        v[k] = bk ? m : v[k];
+        cnt = bk ? T(0) : cnt;
     }
     lam_part += lp;
-    T vv = first;
-    bool fv = hf;
-#pragma unroll
-    for (int d = 1; d < LPR; d <<= 1) {
-        T v2 = shdn<LPR>(vv, d);
-        int f2 = shdn<LPR>((int)fv, d);
-        if (l + d < LPR && !fv) { vv = v2; fv = f2 != 0; }
-    }
-    T cur = shdn<LPR>(vv, 1);
+    T cur = seg_scan_rev<LPR>(fv, fl, l);
 #pragma unroll
     for (int k = E - 1; k >= 0; --k) {
-        if ((bnd >> k) & 1u) cur = v[k]; else v[k] = cur;
+        T x = bit<E>(bnd, k) ? v[k] : cur;
+        x = bit<E>(firstm, k) ? fv : x;
+        v[k] = x;
+        cur = x;
     }
 }
 

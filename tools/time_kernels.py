@@ -1,0 +1,71 @@
+"""Quick device timing of the hot-path calls (CUDA events, warm, no profiler).
+
+    python tools/time_kernels.py [c2|c3|c4|c5|all]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2204_03643_b200 import _lib, tvprox, workloads  # noqa: E402
+
+
+def timeit(fn, reps=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def c2():
+    w = workloads.c2()
+    y = torch.as_tensor(w.y, device="cuda")
+    lam = torch.as_tensor(w.lam.astype(np.float32), device="cuda")
+    g = torch.as_tensor(w.grad, device="cuda")
+    x, mask, it = tvprox.tv1d_fwd(y, lam, want_iters=True)
+    itn = it.cpu().numpy()
+    f = timeit(lambda: tvprox.tv1d_fwd(y, lam))
+    bw = timeit(lambda: tvprox.tv1d_bwd(g, mask, _lib.LAM_PER_ROW))
+    gbs = 65536 * (8192 + 260) / 1e9
+    print("C2 fwd %.3f ms (%.0f GB/s)  bwd %.3f ms (%.0f GB/s)  iters mean %.2f p99 %d max %d nc %d stall %d" % (
+        f, gbs / f * 1e3, bw, gbs / bw * 1e3, (itn & 0xffff).mean(), np.percentile(itn & 0xffff, 99),
+        (itn & 0xffff).max(), (itn < 0).sum(), ((itn > 0) & ((itn >> 16) & 1 == 1)).sum()), flush=True)
+    # stress: iid normal rows
+    ys = torch.randn(65536, 1024, device="cuda")
+    x, mask, it = tvprox.tv1d_fwd(ys, 1.0, want_iters=True)
+    itn = it.cpu().numpy()
+    f = timeit(lambda: tvprox.tv1d_fwd(ys, 1.0))
+    print("C2-stress(iid N(0,1), lam 1) fwd %.3f ms iters mean %.2f max %d" % (f, (itn & 0xffff).mean(), (itn & 0xffff).max()), flush=True)
+
+
+def twod(name):
+    w = getattr(workloads, name)()
+    X = torch.as_tensor(w.X, device="cuda")
+    lam = w.lam_scalar if w.lam_mode == "scalar" else torch.as_tensor(w.lam.astype(np.float32), device="cuda")
+    G = torch.as_tensor(w.grad, device="cuda")
+    mode = {"scalar": 0, "channel": 3, "plane": 4}[w.lam_mode]
+    Y, saved, it = tvprox.tv2d_fwd(X, lam, w.iters, want_iters=True)
+    f = timeit(lambda: tvprox.tv2d_fwd(X, lam, w.iters), reps=5)
+    bw = timeit(lambda: tvprox.tv2d_bwd(G, saved, mode, w.iters), reps=5)
+    px = X.numel()
+    print("%s fwd %.3f ms bwd %.3f ms  -> %.0f Mpx/s fwd+bwd; max iters/pass %s" % (
+        name.upper(), f, bw, px / ((f + bw) * 1e-3) / 1e6, it.cpu().numpy().tolist()), flush=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if which in ("c2", "all"):
+        c2()
+    for n in ("c3", "c4", "c5"):
+        if which in (n, "all"):
+            twod(n)
