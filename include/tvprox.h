@@ -84,6 +84,18 @@ tvp_status_t tv1d_prox_fwd(tvp_dtype_t dt, const void *y, void *x,
                            const void *lam, tvp_lam_mode_t lm, double lam_scalar,
                            uint32_t *mask, int32_t *row_iters, tvp_stream_t stream);
 
+/*
+ * tv1d_prox_fwd_warm -- tv1d_prox_fwd whose projected Newton starts from the
+ * bound set of a previous solve (DESIGN.md a-11): edges coded up/down in
+ * mask_in start bound at +lam/-lam.  The result is the same prox (Eq. 1); only
+ * the iteration count changes.  mask_in may alias mask_out (read before write).
+ */
+tvp_status_t tv1d_prox_fwd_warm(tvp_dtype_t dt, const void *y, void *x,
+                                int64_t batch, int64_t n, int64_t stride,
+                                const void *lam, tvp_lam_mode_t lm, double lam_scalar,
+                                const uint32_t *mask_in, uint32_t *mask_out,
+                                int32_t *row_iters, tvp_stream_t stream);
+
 /* Workspace of tv1d_prox_bwd in bytes (nonzero only for TVP_LAM_SCALAR). */
 size_t tv1d_bwd_workspace_bytes(tvp_dtype_t dt, int64_t batch, tvp_lam_mode_t lm);
 

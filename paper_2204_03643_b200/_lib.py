@@ -51,6 +51,8 @@ def load(path: str = LIB_PATH):
         lib.tv1d_mask_words.restype = u64
         lib.tv1d_prox_fwd.argtypes = [i32, vp, vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp]
         lib.tv1d_prox_fwd.restype = i32
+        lib.tv1d_prox_fwd_warm.argtypes = [i32, vp, vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp, vp]
+        lib.tv1d_prox_fwd_warm.restype = i32
         lib.tv1d_bwd_workspace_bytes.argtypes = [i32, i64, i32]
         lib.tv1d_bwd_workspace_bytes.restype = u64
         lib.tv1d_prox_bwd.argtypes = [i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, vp]

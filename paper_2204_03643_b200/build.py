@@ -42,18 +42,22 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, debug: bool = False) -> str:
+    """debug=True builds libtvprox_debug.so with -DTVP_DEBUG (per-iteration device printf)."""
+    bdir = BUILD + ("_debug" if debug else "")
+    lib = LIB.replace(".so", "_debug.so") if debug else LIB
+    os.makedirs(bdir, exist_ok=True)
     deps = _deps()
-    if not force and not _stale(LIB, deps):
-        return LIB
+    if not force and not _stale(lib, deps):
+        return lib
     objs = []
     jobs = []
     for src in _sources():
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _stale(obj, deps):
-            cmd = [NVCC] + ARCH + FLAGS + (["-Xptxas", "-v"] if ptxas_v else []) + ["-c", src, "-o", obj]
+            cmd = [NVCC] + ARCH + FLAGS + (["-Xptxas", "-v"] if ptxas_v else []) + \
+                (["-DTVP_DEBUG"] if debug else []) + ["-c", src, "-o", obj]
             jobs.append(cmd)
 
     def run(cmd):
@@ -68,14 +72,14 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
                 sys.stderr.write(p.stdout + p.stderr)
             if p.returncode:
                 raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    tmp = LIB + ".tmp%d" % os.getpid()
+    tmp = lib + ".tmp%d" % os.getpid()
     link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs
     p = subprocess.run(link, capture_output=True, text=True)
     if p.returncode:
         sys.stderr.write(p.stdout + p.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
@@ -83,5 +87,6 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ptxas", action="store_true")
+    ap.add_argument("--debug", action="store_true")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose, ptxas_v=a.ptxas))
+    print(build(force=a.force, verbose=a.verbose, ptxas_v=a.ptxas, debug=a.debug))

@@ -24,6 +24,9 @@
 // only runs when the full step would leave the box.
 #pragma once
 #include "tv_common.cuh"
+#ifdef TVP_DEBUG
+#include <cstdio>
+#endif
 
 namespace tvp {
 
@@ -113,20 +116,16 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                                         const Lam<T, E, PE>& lam, int l, bool active) {
     warm_pos &= ~pin;
     warm_neg &= ~pin;
-    T ymax = T(0), lmax = T(0);
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         const T lk = lam.at(k);
         u[k] = bit<E>(warm_pos, k) ? lk : (bit<E>(warm_neg, k) ? -lk : T(0));
-        ymax = fmax(ymax, fabs(y[k]));
-        if (PE) lmax = fmax(lmax, lk);
     }
-    ymax = group_max<LPR>(ymax);
-    lmax = PE ? group_max<LPR>(lmax) : lam.r;
     uint32_t bnd = pin | warm_pos | warm_neg;
+    uint32_t bnd2 = 0xffffffffu;       // bound set two iterations ago (cycle detection)
     const T ynext = shdn<LPR>(y[0], 1);
     const T eps = Num<T>::eps;
-    const T slackA = eps * T(E + 2 * Log2<LPR>::v + 8);   // summation-depth factor of the KKT slack
+    const T slackA = eps * T(8);     // summation-error slack of the KKT test (x sum |terms|)
     const T slack1 = T(1) + T(2) * eps;
     const int maxit = Num<T>::max_iters;
 
@@ -144,7 +143,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         const T uprev = (l == 0) ? T(0) : uprev0;
         const T unext = shdn<LPR>(u[0], 1);
         uint32_t nb = 0;
-        T s = T(0), cnt = T(0), numf = T(0);
+        T s = T(0), cnt = T(0), numf = T(0), ub = T(0);
         bool hf = false;
         T xk = y[0] + u[0] - uprev;
 #pragma unroll
@@ -154,24 +153,27 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                                       : (ynext + unext - u[k]);
             const T g = xk1 - xk;
             xk = xk1;
-            const bool bk = bit<E>(keep, k) || ((fabs(u[k]) >= thr) && (u[k] * g > T(0)));
-            if (bk) nb |= 1u << k;
+            const bool bk = bit<E>(keep, k) | ((fabs(u[k]) >= thr) & (u[k] * g > T(0)));
+            nb |= (uint32_t)bk << k;
             s += y[k];
             cnt += T(1);
             const T num = s + u[k];
             const T val = num * rcp_(cnt);
-            numf = (bk && !hf) ? num : numf;
+            numf = (bk & !hf) ? num : numf;
             w[k] = bk ? (hf ? val : num) : w[k];
-            hf = hf || bk;
+            hf = hf | bk;
+            ub = bk ? u[k] : ub;
             s = bk ? -u[k] : s;
             cnt = bk ? T(0) : cnt;
         }
         const bool bchg = group_any<LPR>(nb != bnd);
-        if (upd && !uchg && !bchg) { stall = true; run = false; }
+        // rounding-level fixed point (no change) or 2-cycle of the bound set: stall
+        const bool cyc2 = bchg & group_all<LPR>(nb == bnd2);
+        if (upd && ((!uchg && !bchg) || cyc2)) { stall = true; run = false; }
+        bnd2 = bnd;
         bnd = nb;
         const int hb = 31 - __clz(bnd);              // -1 if none
         const bool fl = bnd != 0u;
-        const T s_tail = s;                           // sum_y(tail) - u(last bound)
         const int cnt_tail = E - 1 - hb;
         T cs = s;
         int cc = cnt_tail;
@@ -180,15 +182,23 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         // ---------------- P2/P3: the lane's first segment gets the carry; reverse
         // broadcast of each segment's value to its samples.
         const int fb = __ffs(bnd) - 1;                // -1 if none
-        const uint32_t firstm = (bnd & (0u - bnd)) * 2u - 1u;   // bits 0..fb
+        const uint32_t firstm = bnd ? ((bnd & (0u - bnd)) * 2u - 1u) : 0u;   // bits 0..fb
         const T fv = (numf + cs) * rcp_(T(fb + 1 + cc));
         T cur = seg_scan_rev<LPR>(fv, fl, l);
+        // (the same reverse pass sums xhat - y over the lane's open tail: the lane
+        // aggregate of the uhat scan below, accumulated term by term)
+        const uint32_t tailm = fl ? ~((2u << hb) - 1u) : 0xffffffffu;
+        T rt = T(0), at = T(0);
 #pragma unroll
         for (int k = E - 1; k >= 0; --k) {
             T v = bit<E>(bnd, k) ? w[k] : cur;
             v = bit<E>(firstm, k) ? fv : v;
             w[k] = v;
             cur = v;
+            const T t = v - y[k];
+            const bool tk = bit<E>(tailm, k);
+            rt += tk ? t : T(0);
+            at += tk ? fabs(t) : T(0);
         }
         if (fin) break;
 
@@ -196,9 +206,8 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         // uhat_i = u_{a-1} + sum_{j=a..i} (xhat_j - y_j); free edges must satisfy
         // |uhat_i| <= lam_i (up to a summation-error slack), bound edges must jump
         // in the direction of u_i.
-        const T c_tail = w[E - 1];
-        T r = T(cnt_tail) * c_tail - s_tail;
-        T A = T(cnt_tail) * (fabs(c_tail) + ymax) + lmax;
+        T r = ub + rt;
+        T A = fabs(ub) + at;
         seg_scan_fwd2<LPR>(r, A, fl, l);
         const T xnext = shdn<LPR>(w[0], 1);
         bool ok = true, clip = false, chg = false;
@@ -211,12 +220,12 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             A += fabs(t);
             const T lk = lam.at(k);
             const bool bk = bit<E>(bnd, k);
-            const bool sgn_bad = (u[k] * (xh1 - xh) < T(0)) && !bit<E>(pin, k);
+            const bool sgn_bad = (u[k] * (xh1 - xh) < T(0)) & !bit<E>(pin, k);
             const T ar = fabs(r);
             const bool infeas = ar > fma(slackA, A, lk * slack1);
-            ok = ok && !(bk ? sgn_bad : infeas);
-            clip = clip || (!bk && ar > lk);
-            chg = chg || (!bk && r != u[k]);
+            ok = ok & !(bk ? sgn_bad : infeas);
+            clip = clip | (!bk & (ar > lk));
+            chg = chg | (!bk & (r != u[k]));
             w[k] = bk ? u[k] : r;
             A = bk ? fabs(u[k]) : A;
             r = bk ? u[k] : r;
@@ -224,6 +233,11 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         ok = group_all<LPR>(ok);
         clip = group_any<LPR>(clip);
         chg = group_any<LPR>(chg);
+#ifdef TVP_DEBUG
+        if (active && l == 0)
+            printf("[tvp] itw %d it %d run %d first %d ok %d clip %d chg %d bchg %d uchg %d nbound %d\n", itw, it,
+                   (int)run, (int)first, (int)ok, (int)clip, (int)chg, (int)bchg, (int)uchg, __popc(bnd));
+#endif
         if (run) ++it;
         if (run && ok) { conv = true; run = false; }
 
@@ -264,7 +278,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                     F = fma(dl, T(2) * x0 + dl, F);
                     G = fma(g, du, G);
                     S = fma(g, dk, S);
-                    ch = ch || (du != T(0));
+                    ch = ch | (du != T(0));
                     duprev = du;
                     x0 = x1;
                 }
@@ -273,10 +287,15 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                 S = group_sum<LPR>(S);
                 ch = group_any<LPR>(ch);
                 if (trial == 0) slope = S;
+#ifdef TVP_DEBUG
+                if (pending && l == 0) printf("[tvp]   LS trial %d alpha %g F %g G %g S %g ch %d\n", trial, (double)alpha, (double)F, (double)G, (double)S, (int)ch);
+#endif
                 if (pending) {
                     const T gain = T(-0.5) * F;          // phi(u(alpha)) - phi(u)
                     if (gain >= T(1e-4) * G) {
-                        pending = false; accepted = true; lchg = ch;
+                        // an accepted step without measurable ascent is a rounding-level
+                        // fixed point: stall (O8)
+                        pending = false; accepted = gain > T(0); lchg = ch;
                     } else {
                         const T den = T(2) * (slope * alpha - gain);
                         const T an = den > T(0) ? slope * alpha * alpha / den : T(0.5) * alpha;
@@ -334,8 +353,8 @@ __device__ __forceinline__ void seg_mean(T (&v)[E], uint32_t bnd, uint32_t pos, 
     for (int k = 0; k < E; ++k) {
         s += v[k];
         const bool bk = bit<E>(bnd, k);
-        sf = (bk && !hf) ? s : sf;
-        hf = hf || bk;
+        sf = (bk & !hf) ? s : sf;
+        hf = hf | bk;
         v[k] = bk ? s : v[k];
         s = bk ? T(0) : s;
     }
@@ -357,7 +376,7 @@ __device__ __forceinline__ void seg_mean(T (&v)[E], uint32_t bnd, uint32_t pos, 
     int sle = shup<LPR>((slc + 2) | (fs ? 4 : 0), 1);
     const int csl = (l == 0 || !(sle & 4)) ? 0 : ((sle & 3) - 2);
     const int fb = __ffs(bnd) - 1;
-    const uint32_t firstm = (bnd & (0u - bnd)) * 2u - 1u;
+    const uint32_t firstm = bnd ? ((bnd & (0u - bnd)) * 2u - 1u) : 0u;
     const T fv = (sf + cs) * rcp_(T(fb + 1 + cc));
     T lp = T(0);
     int prev_s = csl;

@@ -92,7 +92,7 @@ size_t tv2d_workspace_bytes(tvp_dtype_t dt, int64_t N, int64_t C, int64_t H, int
 template <typename T>
 static tvp_status_t tv1d_fwd_impl(const void* y, void* x, int64_t batch, int64_t n, int64_t stride,
                                   const void* lam, tvp_lam_mode_t lm, double lam_scalar, uint32_t* mask,
-                                  int32_t* row_iters, cudaStream_t s) {
+                                  int32_t* row_iters, cudaStream_t s, const uint32_t* mask_in = nullptr) {
     RowFwdArgs<T> a{};
     a.src0 = static_cast<const T*>(y);
     a.src1 = nullptr;
@@ -106,7 +106,7 @@ static tvp_status_t tv1d_fwd_impl(const void* y, void* x, int64_t batch, int64_t
     a.stride = stride;
     a.lines_per_plane = 1;
     a.C = 1;
-    a.mask_in = nullptr;
+    a.mask_in = mask_in;
     a.mask_out = mask;
     a.mw = (int)mask_words(n);
     a.row_iters = row_iters;
@@ -130,6 +130,27 @@ extern "C" tvp_status_t tv1d_prox_fwd(tvp_dtype_t dt, const void* y, void* x, in
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     return dt == TVP_F32 ? tv1d_fwd_impl<float>(y, x, batch, n, stride, lam, lm, lam_scalar, mask, row_iters, s)
                          : tv1d_fwd_impl<double>(y, x, batch, n, stride, lam, lm, lam_scalar, mask, row_iters, s);
+}
+
+extern "C" tvp_status_t tv1d_prox_fwd_warm(tvp_dtype_t dt, const void* y, void* x, int64_t batch, int64_t n,
+                                           int64_t stride, const void* lam, tvp_lam_mode_t lm, double lam_scalar,
+                                           const uint32_t* mask_in, uint32_t* mask_out, int32_t* row_iters,
+                                           tvp_stream_t stream) {
+    if (n > 1 && batch > 0 && !mask_in) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: NULL mask_in");
+    if (dt != TVP_F32 && dt != TVP_F64) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: bad dtype");
+    if (batch < 0 || n < 1 || stride < n) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: need batch >= 0, n >= 1, stride >= n");
+    if (lm != TVP_LAM_SCALAR && lm != TVP_LAM_PER_ROW && lm != TVP_LAM_PER_EDGE)
+        return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: lam mode must be SCALAR, PER_ROW or PER_EDGE");
+    if (lm == TVP_LAM_SCALAR && !(std::isfinite(lam_scalar) && lam_scalar >= 0.0))
+        return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: lam_scalar must be finite and >= 0");
+    if (batch == 0) return TVP_OK;
+    if (!y || !x) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: NULL y or x");
+    if (lm != TVP_LAM_SCALAR && !lam) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: NULL lam");
+    if (n > kMaxLine) return fail(TVP_EUNSUPPORTED, "tv1d_prox_fwd_warm: n > tvp_max_line()");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    return dt == TVP_F32
+               ? tv1d_fwd_impl<float>(y, x, batch, n, stride, lam, lm, lam_scalar, mask_out, row_iters, s, mask_in)
+               : tv1d_fwd_impl<double>(y, x, batch, n, stride, lam, lm, lam_scalar, mask_out, row_iters, s, mask_in);
 }
 
 template <typename T>

@@ -70,8 +70,10 @@ def _lam1d(lam, y: torch.Tensor):
     raise ValueError("tvprox: lam must be a float, [batch] or [batch, n-1]")
 
 
-def tv1d_fwd(y: torch.Tensor, lam, need_mask: bool = True, want_iters: bool = False):
-    """Batched 1D TV prox forward.  Returns (x, mask or None, row_iters or None)."""
+def tv1d_fwd(y: torch.Tensor, lam, need_mask: bool = True, want_iters: bool = False,
+             warm_mask: torch.Tensor = None):
+    """Batched 1D TV prox forward.  Returns (x, mask or None, row_iters or None).
+    warm_mask: optional saved mask of a previous solve to warm-start projected Newton."""
     _require_cuda(y)
     y = _rows(y)
     dt = _dtype_code(y)
@@ -85,8 +87,13 @@ def tv1d_fwd(y: torch.Tensor, lam, need_mask: bool = True, want_iters: bool = Fa
     mw = lib.tv1d_mask_words(n)
     mask = torch.empty((b, max(mw, 1)), device=y.device, dtype=torch.int32) if need_mask else None
     it = torch.empty(b, device=y.device, dtype=torch.int32) if want_iters else None
-    check(lib.tv1d_prox_fwd(dt, _ptr(y), _ptr(x), b, n, stride, _ptr(lt), mode, scal,
-                            _ptr(mask), _ptr(it), _stream(y)), "tv1d_prox_fwd")
+    if warm_mask is not None:
+        _require_cuda(warm_mask)
+        check(lib.tv1d_prox_fwd_warm(dt, _ptr(y), _ptr(x), b, n, stride, _ptr(lt), mode, scal,
+                                     _ptr(warm_mask), _ptr(mask), _ptr(it), _stream(y)), "tv1d_prox_fwd_warm")
+    else:
+        check(lib.tv1d_prox_fwd(dt, _ptr(y), _ptr(x), b, n, stride, _ptr(lt), mode, scal,
+                                _ptr(mask), _ptr(it), _stream(y)), "tv1d_prox_fwd")
     return x, mask, it
 
 

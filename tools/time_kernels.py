@@ -48,6 +48,23 @@ def c2():
     print("C2-stress(iid N(0,1), lam 1) fwd %.3f ms iters mean %.2f max %d" % (f, (itn & 0xffff).mean(), (itn & 0xffff).max()), flush=True)
 
 
+def sweep():
+    """ns per (sample x PN iteration) of the 1D forward for each register geometry."""
+    rng = np.random.default_rng(0)
+    for n in (32, 56, 64, 128, 224, 256, 512, 1024):
+        rows = (1 << 26) // n
+        y = np.zeros((rows, n), np.float32)
+        y[:, n // 2:] = 1.0
+        y += (rng.standard_normal((rows, n)) * np.where(np.arange(rows) % 2 == 0, 0.1, 0.5)[:, None]).astype(np.float32)
+        yt = torch.as_tensor(y, device="cuda")
+        lam = torch.full((rows,), 0.7 * n / 1024 + 0.05, device="cuda")
+        x, mask, it = tvprox.tv1d_fwd(yt, lam, want_iters=True)
+        itn = (it.cpu().numpy() & 0xffff).astype(np.float64)
+        f = timeit(lambda: tvprox.tv1d_fwd(yt, lam), reps=5)
+        print("n %5d rows %7d fwd %.3f ms  iters mean %.2f max %d  -> %.3f ns/(sample*iter)  %.1f Gsample/s" % (
+            n, rows, f, itn.mean(), itn.max(), f * 1e6 / (rows * n * itn.mean()), rows * n / f / 1e6), flush=True)
+
+
 def twod(name):
     w = getattr(workloads, name)()
     X = torch.as_tensor(w.X, device="cuda")
@@ -64,6 +81,8 @@ def twod(name):
 
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if which in ("sweep",):
+        sweep()
     if which in ("c2", "all"):
         c2()
     for n in ("c3", "c4", "c5"):
