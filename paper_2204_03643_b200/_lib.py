@@ -19,7 +19,8 @@ ITERS_NOT_CONVERGED, ITERS_NONFINITE, ITERS_STALL_FLAG = -1, -2, 1 << 16
 
 # every symbol include/tvprox.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "tvp_max_line", "tv1d_mask_words", "tv1d_prox_fwd", "tv1d_bwd_workspace_bytes", "tv1d_prox_bwd",
+    "tvp_max_line", "tv1d_mask_words", "tv1d_prox_fwd", "tv1d_prox_fwd_warm", "tv1d_bwd_workspace_bytes",
+    "tv1d_prox_bwd",
     "tv2d_saved_bytes", "tv2d_workspace_bytes", "tv2d_prox_fwd", "tv2d_prox_bwd",
     "tvp_status_string", "tvp_last_error", "tvp_version", "tvp_launch_count",
 ]

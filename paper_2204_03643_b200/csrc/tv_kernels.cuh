@@ -557,18 +557,40 @@ struct LamReduceArgs {
     T* out;
     int64_t nout;
     int64_t reps, rep_stride, q_stride, seglen;
+    T* scratch;              // [nout][nchunk] first-level partials
+    int nchunk;              // chunks per output (fixed by the sizes, not the GPU)
 };
 
+// Level 1: block (c, q) sums contributions j in [c*CH, (c+1)*CH) of output q,
+// j enumerating (rep, s) in order; fixed-shape tree -> deterministic.
 template <typename T>
-__global__ void __launch_bounds__(256) k_lam_reduce(LamReduceArgs<T> a) {
+__global__ void __launch_bounds__(256) k_lam_reduce1(LamReduceArgs<T> a) {
+    __shared__ T red[256];
+    const int64_t q = blockIdx.x;
+    const int64_t total = a.reps * a.seglen;
+    const int64_t ch = (total + a.nchunk - 1) / a.nchunk;
+    const int64_t j0 = (int64_t)blockIdx.y * ch, j1 = min(total, j0 + ch);
+    T acc = T(0);
+    for (int64_t j = j0 + threadIdx.x; j < j1; j += 256) {
+        const int64_t rep = j / a.seglen, s = j - rep * a.seglen;
+        acc += a.part[rep * a.rep_stride + q * a.q_stride + s];
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int m = 128; m >= 1; m >>= 1) {
+        if ((int)threadIdx.x < m) red[threadIdx.x] += red[threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.scratch[q * a.nchunk + blockIdx.y] = red[0];
+}
+
+// Level 2: output q = fixed-order sum of its nchunk partials.
+template <typename T>
+__global__ void __launch_bounds__(256) k_lam_reduce2(LamReduceArgs<T> a) {
     __shared__ T red[256];
     for (int64_t q = blockIdx.x; q < a.nout; q += gridDim.x) {
         T acc = T(0);
-        const int64_t total = a.reps * a.seglen;
-        for (int64_t j = threadIdx.x; j < total; j += 256) {
-            int64_t rep = j / a.seglen, s = j - rep * a.seglen;
-            acc += a.part[rep * a.rep_stride + q * a.q_stride + s];
-        }
+        for (int c = threadIdx.x; c < a.nchunk; c += 256) acc += a.scratch[q * a.nchunk + c];
         red[threadIdx.x] = acc;
         __syncthreads();
         for (int m = 128; m >= 1; m >>= 1) {

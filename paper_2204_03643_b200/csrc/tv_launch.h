@@ -26,6 +26,15 @@ inline Geo pick_geo(int64_t n) {
     return {32, 32};
 }
 constexpr int64_t kMaxLine = 1024;
+// First-level chunks of the lambda-gradient reduction: a function of the sizes only
+// (never of the GPU), so results are bitwise reproducible across devices.
+inline int lam_chunks(int64_t total, int64_t nout) {
+    (void)nout;
+    int64_t c = (total + 8191) / 8192;
+    if (c > 512) c = 512;
+    if (c < 1) c = 1;
+    return (int)c;
+}
 
 template <typename T> cudaError_t launch_row_fwd(const RowFwdArgs<T>& a, bool per_edge, bool dykstra, cudaStream_t s);
 template <typename T> cudaError_t launch_col_fwd(ColFwdArgs<T> a, cudaStream_t s);

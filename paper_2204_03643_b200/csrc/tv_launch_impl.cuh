@@ -156,8 +156,11 @@ cudaError_t launch_col_bwd(ColBwdArgs<T> a, cudaStream_t s) {
 template <typename T>
 cudaError_t launch_lam_reduce(const LamReduceArgs<T>& a, cudaStream_t s) {
     if (a.nout <= 0) return cudaSuccess;
-    int grid = (int)std::min<int64_t>(a.nout, 4096);
-    k_lam_reduce<T><<<grid, 256, 0, s>>>(a);
+    dim3 g1((unsigned)a.nout, a.nchunk);
+    k_lam_reduce1<T><<<g1, 256, 0, s>>>(a);
+    count_launch();
+    int g2 = (int)std::min<int64_t>(a.nout, 4096);
+    k_lam_reduce2<T><<<g2, 256, 0, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }

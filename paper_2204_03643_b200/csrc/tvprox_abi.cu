@@ -54,7 +54,8 @@ size_t tv1d_mask_words(int64_t n) { return (size_t)mask_words(n); }
 
 size_t tv1d_bwd_workspace_bytes(tvp_dtype_t dt, int64_t batch, tvp_lam_mode_t lm) {
     if (lm != TVP_LAM_SCALAR || batch <= 0) return 0;
-    return align256((size_t)batch * (dt == TVP_F64 ? 8 : 4));
+    const size_t esz = dt == TVP_F64 ? 8 : 4;
+    return align256((size_t)batch * esz) + align256(512 * esz);
 }
 
 size_t tv2d_saved_bytes(int64_t N, int64_t C, int64_t H, int64_t W, int iters) {
@@ -64,7 +65,7 @@ size_t tv2d_saved_bytes(int64_t N, int64_t C, int64_t H, int64_t W, int iters) {
 }
 
 struct Ws2D {
-    size_t z, p, q, rmask, cmask, lam, total;
+    size_t z, p, q, rmask, cmask, lam, lam2, total;
 };
 static Ws2D ws_layout(size_t esz, int64_t N, int64_t C, int64_t H, int64_t W, int iters) {
     const int64_t planes = N * C;
@@ -77,6 +78,7 @@ static Ws2D ws_layout(size_t esz, int64_t N, int64_t C, int64_t H, int64_t W, in
     w.rmask = off; off += align256((size_t)planes * H * mask_words(W) * 4);
     w.cmask = off; off += align256((size_t)planes * W * mask_words(H) * 4);
     w.lam = off; off += align256((size_t)planes * iters * (H + W) * esz);
+    w.lam2 = off; off += align256((size_t)512 * (planes > 0 ? planes : 1) * esz);
     w.total = off;
     return w;
 }
@@ -185,6 +187,8 @@ static tvp_status_t tv1d_bwd_impl(const void* gx, const uint32_t* mask, void* gy
         r.rep_stride = 0;
         r.q_stride = 0;
         r.seglen = batch;
+        r.nchunk = lam_chunks(batch, 1);
+        r.scratch = reinterpret_cast<T*>(static_cast<char*>(ws) + align256((size_t)batch * sizeof(T)));
         e = launch_lam_reduce<T>(r, s);
     }
     return cuda_status(e, "tv1d_prox_bwd");
@@ -361,6 +365,8 @@ static tvp_status_t tv2d_bwd_impl(const void* GYv, const void* saved, void* GXv,
         } else {
             q.nout = planes; q.reps = 1; q.rep_stride = 0; q.q_stride = per_plane; q.seglen = per_plane;
         }
+        q.nchunk = lam_chunks(q.reps * q.seglen, q.nout);
+        q.scratch = reinterpret_cast<T*>(ws + L.lam2);
         cudaError_t e = launch_lam_reduce<T>(q, s);
         if (e != cudaSuccess) return cuda_status(e, "tv2d_prox_bwd(lam)");
     }
