@@ -137,12 +137,20 @@ def dist_setup(args):
     return ws, rank, local
 
 
-def allreduce_max(x, ws):
+def shard(total, ws, rank):
+    """Contiguous block of `total` independent units (images / rows) owned by `rank`."""
+    base, rem = divmod(total, ws)
+    off = rank * base + min(rank, rem)
+    return off, base + (1 if rank < rem else 0)
+
+
+def allreduce_max(x, ws, device="cuda"):
+    """Max over ranks (the timing rule: the slowest rank sets the step time)."""
     if ws == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -257,8 +265,8 @@ def bench_c2_e2e(args, host, local):
 def bench_c5(args, ws, rank, local):
     import torch
     from paper_2204_03643_b200 import _lib, tvprox, workloads
-    per = 256 // ws
-    w = workloads.c5(N=per, image_offset=rank * per)
+    off, per = shard(256, ws, rank)
+    w = workloads.c5(N=per, image_offset=off)
     dev = torch.device("cuda", local)
     X = torch.as_tensor(w.X, device=dev)
     lam = torch.as_tensor(w.lam.astype(np.float32), device=dev)
