@@ -1,0 +1,192 @@
+// tv_comm.cuh -- line-group communication for the PN solver.
+//
+// A line is held by LPR lanes of each of WPL warps (NL = LPR*WPL lanes, line lane
+// index w*LPR + l).  WPL == 1: the group is LPR consecutive lanes of one warp and
+// every operation is a width-LPR warp shuffle / vote.  WPL > 1: the block is
+// exactly one line (LPR == 32); warp-level results are combined across the WPL
+// warps through a small shared-memory scratch and __syncthreads.  Each call site
+// owns a slot S, so a slot is rewritten only after at least one other barrier.
+#pragma once
+#include "tv_common.cuh"
+
+namespace tvp {
+
+constexpr int kCommSlots = 12;
+
+template <typename T, int LPR, int WPL>
+struct Comm {
+    int l;      // lane within the warp group [0, LPR)
+    int w;      // warp within the line [0, WPL)
+    T* sv;      // [kCommSlots][3][WPL]   (WPL > 1)
+    int* si;    // [kCommSlots][WPL]      (WPL > 1)
+
+    __device__ __forceinline__ bool first_lane() const { return (WPL == 1 || w == 0) && l == 0; }
+    __device__ __forceinline__ T& V(int s, int j, int ww) const { return sv[(s * 3 + j) * WPL + ww]; }
+    __device__ __forceinline__ int& I(int s, int ww) const { return si[s * WPL + ww]; }
+
+    // value held by line lane - 1 (0 at line lane 0)
+    template <int S>
+    __device__ __forceinline__ T prev(T v) const {
+        T p = shup<LPR>(v, 1);
+        if (WPL > 1) {
+            if (l == LPR - 1) V(S, 0, w) = v;
+            __syncthreads();
+            if (l == 0 && w > 0) p = V(S, 0, w - 1);
+        }
+        return first_lane() ? T(0) : p;
+    }
+    // value held by line lane + 1 (unspecified at the last lane)
+    template <int S>
+    __device__ __forceinline__ T next(T v) const {
+        T nx = shdn<LPR>(v, 1);
+        if (WPL > 1) {
+            if (l == 0) V(S, 0, w) = v;
+            __syncthreads();
+            if (l == LPR - 1 && w + 1 < WPL) nx = V(S, 0, w + 1);
+        }
+        return nx;
+    }
+    // both neighbours with one barrier
+    template <int S>
+    __device__ __forceinline__ void prev_next(T vp, T vn, T& p, T& nx) const {
+        p = shup<LPR>(vp, 1);
+        nx = shdn<LPR>(vn, 1);
+        if (WPL > 1) {
+            if (l == LPR - 1) V(S, 0, w) = vp;
+            if (l == 0) V(S, 1, w) = vn;
+            __syncthreads();
+            if (l == 0 && w > 0) p = V(S, 0, w - 1);
+            if (l == LPR - 1 && w + 1 < WPL) nx = V(S, 1, w + 1);
+        }
+        if (first_lane()) p = T(0);
+    }
+
+    __device__ __forceinline__ bool any(bool p) const {
+        if (WPL > 1) return __syncthreads_or(p) != 0;
+        return group_any<LPR>(p);
+    }
+    __device__ __forceinline__ bool all(bool p) const {
+        if (WPL > 1) return __syncthreads_and(p) != 0;
+        return group_all<LPR>(p);
+    }
+    // true iff p on any lane of the warp (loop control; line-uniform values only)
+    __device__ __forceinline__ bool uany(bool p) const {
+        if (WPL > 1) return p;           // block == line: already uniform
+        return __any_sync(FULL, p);
+    }
+
+    template <int S>
+    __device__ __forceinline__ T sum(T v) const {
+        v = group_sum<LPR>(v);
+        if (WPL > 1) {
+            if (l == 0) V(S, 0, w) = v;
+            __syncthreads();
+            v = T(0);
+#pragma unroll
+            for (int i = 0; i < WPL; ++i) v += V(S, 0, i);
+        }
+        return v;
+    }
+    template <int S>
+    __device__ __forceinline__ void sum3(T& a, T& b, T& c) const {
+        a = group_sum<LPR>(a);
+        b = group_sum<LPR>(b);
+        c = group_sum<LPR>(c);
+        if (WPL > 1) {
+            if (l == 0) { V(S, 0, w) = a; V(S, 1, w) = b; V(S, 2, w) = c; }
+            __syncthreads();
+            a = b = c = T(0);
+#pragma unroll
+            for (int i = 0; i < WPL; ++i) { a += V(S, 0, i); b += V(S, 1, i); c += V(S, 2, i); }
+        }
+    }
+    template <int S>
+    __device__ __forceinline__ T max_(T v) const {
+        v = group_max<LPR>(v);
+        if (WPL > 1) {
+            if (l == 0) V(S, 0, w) = v;
+            __syncthreads();
+            v = V(S, 0, 0);
+#pragma unroll
+            for (int i = 1; i < WPL; ++i) v = max(v, V(S, 0, i));
+        }
+        return v;
+    }
+
+    // Segmented exclusive scan of (a, c) with flag f: combine(L, R) = R.f ? R : (L.a + R.a, L.c + R.c).
+    template <int S>
+    __device__ __forceinline__ void scan_fwd(T& a, int& c, bool f) const {
+#pragma unroll
+        for (int d = 1; d < LPR; d <<= 1) {
+            T a2 = shup<LPR>(a, d);
+            int cf2 = shup<LPR>(c | (f ? (1 << 30) : 0), d);
+            if (l >= d && !f) { a += a2; c += cf2 & 0x3fffffff; f = (cf2 >> 30) & 1; }
+        }
+        T ea = shup<LPR>(a, 1);
+        int ecf = shup<LPR>(c | (f ? (1 << 30) : 0), 1);
+        if (l == 0) { ea = T(0); ecf = 0; }
+        if (WPL > 1) {
+            if (l == LPR - 1) { V(S, 0, w) = a; I(S, w) = c | (f ? (1 << 30) : 0); }
+            __syncthreads();
+            T ca = T(0);
+            int cc = 0;
+            for (int i = 0; i < w; ++i) {
+                const T ra = V(S, 0, i);
+                const int rcf = I(S, i);
+                if (rcf >> 30) { ca = ra; cc = rcf & 0x3fffffff; } else { ca += ra; cc += rcf & 0x3fffffff; }
+            }
+            if (!(ecf >> 30)) { ea += ca; ecf += cc; }
+        }
+        a = ea;
+        c = ecf & 0x3fffffff;
+    }
+    // Segmented exclusive scan of two summed values (a, b).
+    template <int S>
+    __device__ __forceinline__ void scan_fwd2(T& a, T& b, bool f) const {
+#pragma unroll
+        for (int d = 1; d < LPR; d <<= 1) {
+            T a2 = shup<LPR>(a, d), b2 = shup<LPR>(b, d);
+            int f2 = shup<LPR>((int)f, d);
+            if (l >= d && !f) { a += a2; b += b2; f = f2 != 0; }
+        }
+        T ea = shup<LPR>(a, 1), eb = shup<LPR>(b, 1);
+        int ef = shup<LPR>((int)f, 1);
+        if (l == 0) { ea = T(0); eb = T(0); ef = 0; }
+        if (WPL > 1) {
+            if (l == LPR - 1) { V(S, 0, w) = a; V(S, 1, w) = b; I(S, w) = (int)f; }
+            __syncthreads();
+            T ca = T(0), cb = T(0);
+            for (int i = 0; i < w; ++i) {
+                if (I(S, i)) { ca = V(S, 0, i); cb = V(S, 1, i); } else { ca += V(S, 0, i); cb += V(S, 1, i); }
+            }
+            if (!ef) { ea += ca; eb += cb; }
+        }
+        a = ea;
+        b = eb;
+    }
+    // Value of the nearest flagged line lane strictly to the right (0 if none).
+    template <int S>
+    __device__ __forceinline__ T scan_rev(T v, bool f) const {
+#pragma unroll
+        for (int d = 1; d < LPR; d <<= 1) {
+            T v2 = shdn<LPR>(v, d);
+            int f2 = shdn<LPR>((int)f, d);
+            if (l + d < LPR && !f) { v = v2; f = f2 != 0; }
+        }
+        T e = shdn<LPR>(v, 1);
+        int ef = shdn<LPR>((int)f, 1);
+        if (l + 1 >= LPR) { e = T(0); ef = 0; }
+        if (WPL > 1) {
+            if (l == 0) { V(S, 0, w) = v; I(S, w) = (int)f; }
+            __syncthreads();
+            if (!ef) {
+                for (int i = w + 1; i < WPL; ++i) {
+                    if (I(S, i)) { e = V(S, 0, i); break; }
+                }
+            }
+        }
+        return e;
+    }
+};
+
+}  // namespace tvp

@@ -113,15 +113,17 @@ __device__ __forceinline__ void smem_to_regs(const T* buf, int l, T (&y)[E]) {
 // Solve one line held by this lane group: centring, pinning, non-finite
 // detection, PN solve.  Writes the uncentred output into `w` and returns the
 // status (row_iters code).
-template <typename T, int E, int LPR, bool PE>
+template <typename T, int E, int LPR, int WPL, bool PE>
 __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& lam, int n,
-                                          bool valid, uint32_t warm_pos, uint32_t warm_neg, int l) {
+                                          bool valid, uint32_t warm_pos, uint32_t warm_neg,
+                                          const Comm<T, LPR, WPL>& C) {
+    const int ll = C.w * LPR + C.l;           // line lane
     uint32_t pin = 0;
     bool bad = false;
     T sum = T(0);
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-        int i = l * E + k;
+        int i = ll * E + k;
         T lk = lam.at(k);
         bool pk = (i >= n - 1) || !(lk > T(0));
         pin |= (pk ? 1u : 0u) << k;
@@ -131,16 +133,16 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
         }
         if (i < n - 1) bad = bad || !finite_(lk) || (lk < T(0));
     }
-    bad = group_any<LPR>(bad);
+    bad = C.any(bad);
     constexpr uint32_t allm = (E == 32) ? 0xffffffffu : ((1u << (E & 31)) - 1u);
-    bool allpin = group_all<LPR>(pin == allm);
-    sum = group_sum<LPR>(sum);
+    bool allpin = C.all(pin == allm);
+    sum = C.template sum<8>(sum);
     bool active = valid && !bad && !allpin;
     T mean = active ? sum / T(n) : T(0);
 #pragma unroll
     for (int k = 0; k < E; ++k) y[k] -= mean;
     T u[E];
-    int st = pn_solve<T, E, LPR, PE>(y, u, w, pin, warm_pos, warm_neg, lam, l, active);
+    int st = pn_solve<T, E, LPR, WPL, PE>(y, u, w, pin, warm_pos, warm_neg, lam, C, active);
 #pragma unroll
     for (int k = 0; k < E; ++k) w[k] = active ? w[k] + mean : (bad ? nan_<T>() : y[k]);
     if (!active) st = bad ? -2 : 0;
@@ -213,7 +215,8 @@ k_row_fwd(RowFwdArgs<T> a) {
             uint32_t wb;
             mask_window<E>(a.mask_in + r * a.mw, a.mw, l * E, wb, wp, wn);
         }
-        int st = solve_line<T, E, LPR, PE>(y, w, lam, n, valid, wp, wn, l);
+        const Comm<T, LPR, 1> C{l, 0, nullptr, nullptr};
+        int st = solve_line<T, E, LPR, 1, PE>(y, w, lam, n, valid, wp, wn, C);
         __syncwarp();
         if (valid) {
 #pragma unroll
@@ -257,6 +260,100 @@ k_row_fwd(RowFwdArgs<T> a) {
             if (a.iters_max) atomicMax(a.iters_max, st >= 0 ? (st & 0xffff) : (1 << 20));
         }
         __syncwarp();
+    }
+}
+
+// ===========================================================================
+// Row forward with WPL warps per line (E samples per lane, 32*WPL lanes per line):
+// the block is one line at a time; cross-warp scans through shared memory.
+// ===========================================================================
+template <typename T, int E, int WPL, bool PE, bool DYK>
+__global__ void __launch_bounds__(WPL * 32)
+k_row_fwd_w(RowFwdArgs<T> a) {
+    constexpr int NT = WPL * 32;
+    constexpr int LP = line_pitch<E, NT>();
+    extern __shared__ __align__(16) unsigned char smraw_[];
+    T* bufA = reinterpret_cast<T*>(smraw_);
+    T* bufX = DYK ? bufA + LP : bufA;
+    __shared__ T comm_v[kCommSlots * 3 * WPL];
+    __shared__ int comm_i[kCommSlots * WPL];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Comm<T, 32, WPL> C{lane, warp, comm_v, comm_i};
+    const int ll = threadIdx.x;                 // line lane
+    const int n = a.n;
+    for (int64_t r = blockIdx.x; r < a.nlines; r += gridDim.x) {
+        const T* s0 = a.src0 + r * a.stride;
+        const T* s1 = (DYK && a.src1) ? a.src1 + r * a.stride : nullptr;
+        {
+            T v0[E], v1[E];
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int i = q * NT + ll;
+                const bool in = i < n;
+                v0[q] = in ? __ldg(s0 + i) : T(0);
+                v1[q] = (DYK && s1 && in) ? __ldg(s1 + i) : T(0);
+            }
+#pragma unroll
+            for (int q = 0; q < E; ++q) bufA[spad(q * NT + ll)] = DYK ? v0[q] + v1[q] : v0[q];
+        }
+        __syncthreads();
+        T y[E], w[E];
+        smem_to_regs<T, E>(bufA, ll, y);
+        Lam<T, E, PE> lam;
+        if (PE) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                int e = ll * E + k;
+                lam.e[PE ? k : 0] = (e < n - 1) ? __ldg(a.lam + r * a.stride + e) : T(0);
+            }
+            lam.r = T(0);
+        } else {
+            lam.r = line_lambda(a.lam, a.lam_mode, a.lam_scalar, r, a.lines_per_plane, a.C);
+        }
+        uint32_t wp = 0, wn = 0;
+        if (a.mask_in && a.mw > 0) {
+            uint32_t wb;
+            mask_window<E>(a.mask_in + r * a.mw, a.mw, ll * E, wb, wp, wn);
+        }
+        int st = solve_line<T, E, 32, WPL, PE>(y, w, lam, n, true, wp, wn, C);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            int i = ll * E + k;
+            if (i < n) bufX[spad(i)] = w[k];
+        }
+        __syncthreads();
+        T* d0 = a.dst0 + r * a.stride;
+        T* d1 = DYK && a.dst1 ? a.dst1 + r * a.stride : nullptr;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            const int i = q * NT + ll;
+            if (i < n) {
+                T xv = bufX[spad(i)];
+                d0[i] = xv;
+                if (DYK && d1) d1[i] = bufA[spad(i)] - xv;
+            }
+        }
+        if (a.mask_out) {
+            T lz_line = PE ? T(1) : line_lambda(a.lam, a.lam_mode, a.lam_scalar, r, a.lines_per_plane, a.C);
+            for (int wd = ll; wd < a.mw; wd += NT) {
+                uint32_t word = 0;
+#pragma unroll 4
+                for (int q = 0; q < 16; ++q) {
+                    int e = wd * 16 + q;
+                    if (e < n - 1) {
+                        T le = PE ? __ldg(a.lam + r * a.stride + e) : lz_line;
+                        word |= edge_code(bufX[spad(e)], bufX[spad(e + 1)], !(le > T(0))) << (2 * q);
+                    }
+                }
+                a.mask_out[r * a.mw + wd] = word;
+            }
+        }
+        if (ll == 0) {
+            if (a.row_iters) a.row_iters[r] = st;
+            if (a.iters_max) atomicMax(a.iters_max, st >= 0 ? (st & 0xffff) : (1 << 20));
+        }
+        __syncthreads();
     }
 }
 
@@ -321,7 +418,8 @@ k_col_fwd(ColFwdArgs<T> a) {
                 uint32_t wb;
                 mask_window<E>(a.mask_in + (p * W + c0 + c) * a.mw, a.mw, l * E, wb, wp, wn);
             }
-            int st = solve_line<T, E, LPR, false>(y, w, lam, H, valid, wp, wn, l);
+            const Comm<T, LPR, 1> C{l, 0, nullptr, nullptr};
+            int st = solve_line<T, E, LPR, 1, false>(y, w, lam, H, valid, wp, wn, C);
             if (valid) {
 #pragma unroll
                 for (int k = 0; k < E; ++k) {

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <mutex>
 #include <unordered_map>
+#include <cstdlib>
 
 #include "tv_kernels.cuh"
 #include "tv_launch.h"
@@ -59,6 +60,18 @@ static int persistent_grid(K kern, int threads, size_t smem, int64_t work_blocks
     } while (0)
 
 constexpr int kRowWPB = 4;
+
+// TVP_ROW_SPLIT selects the row-forward geometry for long lines (A/B measurements):
+// 0 = one warp per line, 2 = two warps per line (default), 4 = four warps per line.
+static int row_fwd_split() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TVP_ROW_SPLIT");
+        v = e ? atoi(e) : 2;
+        if (v != 0 && v != 2 && v != 4) v = 2;
+    }
+    return v;
+}
 constexpr int kColWPB = 8;
 
 template <typename T, int E, int LPR, bool PE, bool DYK>
@@ -74,9 +87,36 @@ static cudaError_t row_fwd_t(const RowFwdArgs<T>& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <typename T, int E, int WPL, bool PE, bool DYK>
+static cudaError_t row_fwd_w_t(const RowFwdArgs<T>& a, cudaStream_t s) {
+    constexpr int LP = line_pitch<E, 32 * WPL>();
+    const size_t smem = (size_t)(DYK ? 2 : 1) * LP * sizeof(T);
+    auto kern = k_row_fwd_w<T, E, WPL, PE, DYK>;
+    const int grid = persistent_grid(kern, WPL * 32, smem, a.nlines);
+    kern<<<grid, WPL * 32, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_row_fwd(const RowFwdArgs<T>& a, bool per_edge, bool dykstra, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
+    const int split = row_fwd_split();
+    if (a.n > 512 && split == 2) {               // 1024-sample lines: two warps x 16 samples per lane
+        if (dykstra) return row_fwd_w_t<T, 16, 2, false, true>(a, s);
+        if (per_edge) return row_fwd_w_t<T, 16, 2, true, false>(a, s);
+        return row_fwd_w_t<T, 16, 2, false, false>(a, s);
+    }
+    if (a.n > 512 && split == 4) {               // four warps x 8 samples per lane
+        if (dykstra) return row_fwd_w_t<T, 8, 4, false, true>(a, s);
+        if (per_edge) return row_fwd_w_t<T, 8, 4, true, false>(a, s);
+        return row_fwd_w_t<T, 8, 4, false, false>(a, s);
+    }
+    if (a.n > 256 && a.n <= 512 && split == 4) { // 512-sample lines: two warps x 8
+        if (dykstra) return row_fwd_w_t<T, 8, 2, false, true>(a, s);
+        if (per_edge) return row_fwd_w_t<T, 8, 2, true, false>(a, s);
+        return row_fwd_w_t<T, 8, 2, false, false>(a, s);
+    }
     TVP_GEO_DISPATCH(a.n, {
         if (dykstra) e = row_fwd_t<T, E_, L_, false, true>(a, s);
         else if (per_edge) e = row_fwd_t<T, E_, L_, true, false>(a, s);

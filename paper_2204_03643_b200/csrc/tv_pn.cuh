@@ -24,6 +24,7 @@
 // only runs when the full step would leave the box.
 #pragma once
 #include "tv_common.cuh"
+#include "tv_comm.cuh"
 #ifdef TVP_DEBUG
 #include <cstdio>
 #endif
@@ -110,10 +111,11 @@ template <> __device__ __forceinline__ double big_<double>() { return 1.0e300; }
 // of the line (slack bound).  Returns the line status: iterations (| 1<<16 if
 // accepted at a stall), or -1 (max iterations, w = x(u)).
 // ---------------------------------------------------------------------------
-template <typename T, int E, int LPR, bool PE>
+template <typename T, int E, int LPR, int WPL, bool PE>
 __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], uint32_t pin,
                                         uint32_t warm_pos, uint32_t warm_neg,
-                                        const Lam<T, E, PE>& lam, int l, bool active) {
+                                        const Lam<T, E, PE>& lam, const Comm<T, LPR, WPL>& C,
+                                        bool active) {
     warm_pos &= ~pin;
     warm_neg &= ~pin;
 #pragma unroll
@@ -123,7 +125,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
     }
     uint32_t bnd = pin | warm_pos | warm_neg;
     uint32_t bnd2 = 0xffffffffu;       // bound set two iterations ago (cycle detection)
-    const T ynext = shdn<LPR>(y[0], 1);
+    const T ynext = C.template next<1>(y[0]);
     const T eps = Num<T>::eps;
     const T slackA = eps * T(8);     // summation-error slack of the KKT test (x sum |terms|)
     const T slack1 = T(1) + T(2) * eps;
@@ -139,9 +141,8 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         //   xhat = (sum_y - u_{a-1} + u_{b-1}) / len ;  s carries sum_y - u_{a-1}.
         const bool upd = run && !first && !fin;
         const uint32_t keep = upd ? pin : bnd;
-        const T uprev0 = shup<LPR>(u[E - 1], 1);
-        const T uprev = (l == 0) ? T(0) : uprev0;
-        const T unext = shdn<LPR>(u[0], 1);
+        T uprev, unext;
+        C.template prev_next<0>(u[E - 1], u[0], uprev, unext);
         uint32_t nb = 0;
         T s = T(0), cnt = T(0), numf = T(0), ub = T(0);
         bool hf = false;
@@ -166,9 +167,9 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             s = bk ? -u[k] : s;
             cnt = bk ? T(0) : cnt;
         }
-        const bool bchg = group_any<LPR>(nb != bnd);
+        const bool bchg = C.any(nb != bnd);
         // rounding-level fixed point (no change) or 2-cycle of the bound set: stall
-        const bool cyc2 = bchg & group_all<LPR>(nb == bnd2);
+        const bool cyc2 = bchg & C.all(nb == bnd2);
         if (upd && ((!uchg && !bchg) || cyc2)) { stall = true; run = false; }
         bnd2 = bnd;
         bnd = nb;
@@ -177,14 +178,14 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         const int cnt_tail = E - 1 - hb;
         T cs = s;
         int cc = cnt_tail;
-        seg_scan_fwd<LPR>(cs, cc, fl, l);
+        C.template scan_fwd<2>(cs, cc, fl);
 
         // ---------------- P2/P3: the lane's first segment gets the carry; reverse
         // broadcast of each segment's value to its samples.
         const int fb = __ffs(bnd) - 1;                // -1 if none
         const uint32_t firstm = bnd ? ((bnd & (0u - bnd)) * 2u - 1u) : 0u;   // bits 0..fb
         const T fv = (numf + cs) * rcp_(T(fb + 1 + cc));
-        T cur = seg_scan_rev<LPR>(fv, fl, l);
+        T cur = C.template scan_rev<3>(fv, fl);
         // (the same reverse pass sums xhat - y over the lane's open tail: the lane
         // aggregate of the uhat scan below, accumulated term by term)
         const uint32_t tailm = fl ? ~((2u << hb) - 1u) : 0xffffffffu;
@@ -208,8 +209,8 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         // in the direction of u_i.
         T r = ub + rt;
         T A = fabs(ub) + at;
-        seg_scan_fwd2<LPR>(r, A, fl, l);
-        const T xnext = shdn<LPR>(w[0], 1);
+        C.template scan_fwd2<4>(r, A, fl);
+        const T xnext = C.template next<5>(w[0]);
         bool ok = true, clip = false, chg = false;
 #pragma unroll
         for (int k = 0; k < E; ++k) {
@@ -230,11 +231,11 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             A = bk ? fabs(u[k]) : A;
             r = bk ? u[k] : r;
         }
-        ok = group_all<LPR>(ok);
-        clip = group_any<LPR>(clip);
-        chg = group_any<LPR>(chg);
+        ok = C.all(ok);
+        clip = C.any(clip);
+        chg = C.any(chg);
 #ifdef TVP_DEBUG
-        if (active && l == 0)
+        if (active && C.first_lane())
             printf("[tvp] itw %d it %d run %d first %d ok %d clip %d chg %d bchg %d uchg %d nbound %d\n", itw, it,
                    (int)run, (int)first, (int)ok, (int)clip, (int)chg, (int)bchg, (int)uchg, __popc(bnd));
 #endif
@@ -253,16 +254,15 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             uchg = chg || first;
         }
         bool pending = run && !fast;
-        if (__any_sync(FULL, pending)) {
+        if (C.uany(pending)) {
             T alpha = T(1), slope = T(0);
             bool accepted = false, lchg = false;
             for (int trial = 0; trial < 30; ++trial) {
-                if (!__any_sync(FULL, pending)) break;
+                if (!C.uany(pending)) break;
                 const T lkl = lam.at(E - 1);
                 const T dlast = bit<E>(bnd, E - 1) ? T(0)
                                                    : clampv(u[E - 1] + alpha * (w[E - 1] - u[E - 1]), -lkl, lkl) - u[E - 1];
-                const T dp0 = shup<LPR>(dlast, 1);
-                T duprev = (l == 0) ? T(0) : dp0;
+                T duprev = C.template prev<6>(dlast);
                 T F = T(0), G = T(0), S = T(0);
                 bool ch = false;
                 T x0 = y[0] + u[0] - uprev;
@@ -282,13 +282,11 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                     duprev = du;
                     x0 = x1;
                 }
-                F = group_sum<LPR>(F);
-                G = group_sum<LPR>(G);
-                S = group_sum<LPR>(S);
-                ch = group_any<LPR>(ch);
+                C.template sum3<7>(F, G, S);
+                ch = C.any(ch);
                 if (trial == 0) slope = S;
 #ifdef TVP_DEBUG
-                if (pending && l == 0) printf("[tvp]   LS trial %d alpha %g F %g G %g S %g ch %d\n", trial, (double)alpha, (double)F, (double)G, (double)S, (int)ch);
+                if (pending && C.first_lane()) printf("[tvp]   LS trial %d alpha %g F %g G %g S %g ch %d\n", trial, (double)alpha, (double)F, (double)G, (double)S, (int)ch);
 #endif
                 if (pending) {
                     const T gain = T(-0.5) * F;          // phi(u(alpha)) - phi(u)
@@ -320,12 +318,11 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             }
         }
         first = false;
-        if (!__any_sync(FULL, run) || itw + 2 >= maxit) fin = true;
+        if (!C.uany(run) || itw + 2 >= maxit) fin = true;
     }
     // lines still running hit max_iters: output the primal of the current dual
-    const T up0 = shup<LPR>(u[E - 1], 1);
+    const T upv = C.template prev<10>(u[E - 1]);
     if (run) {
-        const T upv = (l == 0) ? T(0) : up0;
 #pragma unroll
         for (int k = 0; k < E; ++k) w[k] = y[k] + u[k] - (k > 0 ? u[k > 0 ? k - 1 : 0] : upv);
         return -1;
