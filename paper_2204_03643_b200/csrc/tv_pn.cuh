@@ -100,6 +100,10 @@ __device__ __forceinline__ T seg_scan_rev(T v, bool f, int l) {
     return (l + 1 < LPR) ? e : T(0);
 }
 
+// Iterations after which a line switches from projected full Newton steps to the
+// projected Armijo line search (DESIGN.md a-7).
+constexpr int kLsAfter = 12;
+
 template <typename T> __device__ __forceinline__ T big_();
 template <> __device__ __forceinline__ float big_<float>() { return 3.0e38f; }
 template <> __device__ __forceinline__ double big_<double>() { return 1.0e300; }
@@ -244,7 +248,10 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
 
         // ---------------- step: full Newton step when it stays in the box, else
         // projected Armijo line search with quadratic-interpolation backtracking.
-        const bool fast = run && (first || !clip);
+        // The projected full Newton step clip(u + d) is taken directly; the Armijo
+        // backtracking line search of P:188 is the globalisation safeguard, engaged
+        // for lines that have not converged after kLsAfter iterations.
+        const bool fast = run && (first || !clip || it < kLsAfter);
         if (fast) {
 #pragma unroll
             for (int k = 0; k < E; ++k) {
