@@ -267,8 +267,11 @@ k_row_fwd(RowFwdArgs<T> a) {
 // Row forward with WPL warps per line (E samples per lane, 32*WPL lanes per line):
 // the block is one line at a time; cross-warp scans through shared memory.
 // ===========================================================================
+#ifndef TVP_ROWW_MINB
+#define TVP_ROWW_MINB 1
+#endif
 template <typename T, int E, int WPL, bool PE, bool DYK>
-__global__ void __launch_bounds__(WPL * 32)
+__global__ void __launch_bounds__(WPL * 32, TVP_ROWW_MINB)
 k_row_fwd_w(RowFwdArgs<T> a) {
     constexpr int NT = WPL * 32;
     constexpr int LP = line_pitch<E, NT>();
