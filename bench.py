@@ -351,8 +351,8 @@ def run_ours(args):
     bwd_gbs = bwd_bytes / (r["bwd_ms"] * 1e-3) / 1e9
     dom = "fwd" if r["fwd_ms"] >= r["bwd_ms"] else "bwd"
     roof = {
-        "kernel": "k_row_fwd<float,32,32> (1D projected-Newton forward)" if dom == "fwd"
-        else "k_row_bwd<float,32,32> (1D segment-mean backward)",
+        "kernel": "k_row_fwd_w<float,16,2> (1D projected-Newton forward, 2 warps/line)" if dom == "fwd"
+        else "k_row_bwd (1D segment-mean backward)",
         "bound": "hbm", "achieved": fwd_gbs if dom == "fwd" else bwd_gbs, "peak": peak, "unit": "GB/s",
         "frac": (fwd_gbs if dom == "fwd" else bwd_gbs) / peak, "peak_source": peak_src,
         "traffic": traffic.get("c2_fwd_bytes_per_launch" if dom == "fwd" else "c2_bwd_bytes_per_launch"),
