@@ -164,6 +164,30 @@ struct Comm {
         a = ea;
         b = eb;
     }
+    // Value of the nearest flagged line lane strictly to the left (0 if none).
+    template <int S>
+    __device__ __forceinline__ int scan_last(int v, bool f) const {
+#pragma unroll
+        for (int d = 1; d < LPR; d <<= 1) {
+            int v2 = shup<LPR>(v, d);
+            int f2 = shup<LPR>((int)f, d);
+            if (l >= d && !f) { v = v2; f = f2 != 0; }
+        }
+        int e = shup<LPR>(v, 1);
+        int ef = shup<LPR>((int)f, 1);
+        if (l == 0) { e = 0; ef = 0; }
+        if (WPL > 1) {
+            if (l == LPR - 1) { I(S, w) = f ? ((v + 2) | (1 << 30)) : 0; }   // small ints only
+            __syncthreads();
+            if (!ef) {
+                for (int i = w - 1; i >= 0; --i) {
+                    const int q = I(S, i);
+                    if (q >> 30) { e = (q & 0xffff) - 2; break; }
+                }
+            }
+        }
+        return e;
+    }
     // Value of the nearest flagged line lane strictly to the right (0 if none).
     template <int S>
     __device__ __forceinline__ T scan_rev(T v, bool f) const {

@@ -89,29 +89,40 @@ __device__ __forceinline__ uint32_t edge_code(T xl, T xr, bool lam_zero) {
     return xr > xl ? CODE_UP : (xr < xl ? CODE_DOWN : (lam_zero ? CODE_BOUNDARY : CODE_FUSED));
 }
 
+// Gather the even bits of x (bits 0, 2, ..., 30) into bits 0..15.
+__device__ __forceinline__ uint32_t compact_even(uint32_t x) {
+    x &= 0x55555555u;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0f0f0f0fu;
+    x = (x | (x >> 4)) & 0x00ff00ffu;
+    x = (x | (x >> 8)) & 0x0000ffffu;
+    return x;
+}
+
 // Extract the 2E-bit window of mask codes for edges [e0, e0+E) of one line
 // (word array `mw`, nw words).  Returns per-edge bitmasks: bnd = code != 0,
-// neg = code == DOWN, pos = code == UP.
+// neg = code == DOWN, pos = code == UP (bit-parallel: lo/hi code bits, then
+// even-bit compaction, 16 edges per step).
 template <int E>
 __device__ __forceinline__ void mask_window(const uint32_t* __restrict__ mw, int nw, int e0,
                                             uint32_t& bnd, uint32_t& pos, uint32_t& neg) {
-    bnd = pos = neg = 0;
-    int w0 = e0 >> 4;
-    int sh = (e0 & 15) * 2;
+    const int w0 = e0 >> 4;
+    const int sh = (e0 & 15) * 2;
     constexpr int NS = (2 * E + 31) / 32;   // words of the aligned window
     uint32_t words[NS + 1];
 #pragma unroll
     for (int j = 0; j <= NS; ++j) words[j] = (w0 + j < nw) ? __ldg(mw + w0 + j) : 0u;
-    uint32_t s[NS];
+    bnd = pos = neg = 0;
 #pragma unroll
-    for (int j = 0; j < NS; ++j) s[j] = __funnelshift_r(words[j], words[j + 1], sh);
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-        uint32_t c = (s[(2 * k) >> 5] >> ((2 * k) & 31)) & 3u;
-        bnd |= (c != 0u ? 1u : 0u) << k;
-        pos |= (c == CODE_UP ? 1u : 0u) << k;
-        neg |= (c == CODE_DOWN ? 1u : 0u) << k;
+    for (int j = 0; j < NS; ++j) {
+        const uint32_t c = __funnelshift_r(words[j], words[j + 1], sh);   // 16 codes
+        const uint32_t lo = compact_even(c), hi = compact_even(c >> 1);
+        bnd |= (lo | hi) << (16 * j);
+        pos |= (lo & ~hi) << (16 * j);
+        neg |= (hi & ~lo) << (16 * j);
     }
+    constexpr uint32_t m = (E >= 32) ? 0xffffffffu : ((1u << (E & 31)) - 1u);
+    bnd &= m; pos &= m; neg &= m;
 }
 
 }  // namespace tvp

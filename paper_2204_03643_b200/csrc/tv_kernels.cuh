@@ -573,6 +573,100 @@ k_row_bwd(RowBwdArgs<T> a) {
 }
 
 // ===========================================================================
+// Row backward, one line per block of 32*WPL threads (long lines): each thread
+// holds E contiguous samples loaded straight from HBM into registers (16-byte
+// vector loads when aligned), segment mean through the Comm group, 16-byte
+// stores.  No shared-memory staging.
+// ===========================================================================
+template <typename T, int E>
+__device__ __forceinline__ void ld_contig(const T* __restrict__ p, int i0, int n, bool vec, T (&v)[E]) {
+    if (sizeof(T) == 4 && (E % 4) == 0 && vec && i0 + E <= n) {
+#pragma unroll
+        for (int q = 0; q < E / 4; ++q) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(p + i0) + q);
+            v[4 * q + 0] = (T)f.x; v[4 * q + 1] = (T)f.y; v[4 * q + 2] = (T)f.z; v[4 * q + 3] = (T)f.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = (i0 + k < n) ? __ldg(p + i0 + k) : T(0);
+    }
+}
+template <typename T, int E>
+__device__ __forceinline__ void st_contig(T* __restrict__ p, int i0, int n, bool vec, const T (&v)[E]) {
+    if (sizeof(T) == 4 && (E % 4) == 0 && vec && i0 + E <= n) {
+#pragma unroll
+        for (int q = 0; q < E / 4; ++q)
+            reinterpret_cast<float4*>(p + i0)[q] = make_float4((float)v[4 * q], (float)v[4 * q + 1],
+                                                              (float)v[4 * q + 2], (float)v[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+            if (i0 + k < n) p[i0 + k] = v[k];
+    }
+}
+
+template <typename T, int E, int WPL, bool DYK, bool PE>
+__global__ void __launch_bounds__(WPL * 32)
+k_row_bwd_w(RowBwdArgs<T> a) {
+    __shared__ T comm_v[kCommSlots * 3 * WPL];
+    __shared__ int comm_i[kCommSlots * WPL];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Comm<T, 32, WPL> C{lane, warp, comm_v, comm_i};
+    const int ll = threadIdx.x;
+    const int n = a.n;
+    const int i0 = ll * E;
+    const bool vec = ((a.stride & 3) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(a.out) | reinterpret_cast<uintptr_t>(DYK ? a.B : a.A) |
+                       reinterpret_cast<uintptr_t>(DYK && a.A ? a.A : a.out)) & 15) == 0;
+    for (int64_t r = blockIdx.x; r < a.nlines; r += gridDim.x) {
+        T v[E], pb[E];
+        if (DYK) {
+            ld_contig<T, E>(a.B + r * a.stride, i0, n, vec, v);
+            if (a.A) {
+                ld_contig<T, E>(a.A + r * a.stride, i0, n, vec, pb);
+#pragma unroll
+                for (int k = 0; k < E; ++k) v[k] -= pb[k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < E; ++k) pb[k] = T(0);
+            }
+        } else {
+            ld_contig<T, E>(a.A + r * a.stride, i0, n, vec, v);
+        }
+        uint32_t bnd = 0, pos = 0, neg = 0;
+        if (a.mw > 0) mask_window<E>(a.mask + r * a.mw, a.mw, i0, bnd, pos, neg);
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+            if (i0 + k >= n - 1) bnd |= 1u << k;
+        T lp = T(0);
+        seg_mean_c<T, E, 32, WPL>(v, bnd, pos, neg, C, lp);
+        if (PE) {
+            const T vn = C.template next<4>(v[0]);
+            if (a.lam_edge) {
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    const int e = i0 + k;
+                    const T nxt = (k + 1 < E) ? v[(k + 1 < E) ? k + 1 : k] : vn;
+                    if (e < n - 1) {
+                        const T sg = bit<E>(pos, k) ? T(1) : (bit<E>(neg, k) ? T(-1) : T(0));
+                        a.lam_edge[r * a.stride + e] = sg * (v[k] - nxt);
+                    }
+                }
+            }
+        }
+        if (a.lam_line) {
+            lp = C.template sum<5>(lp);
+            if (ll == 0) a.lam_line[(r / a.lam_lpp) * a.lam_pstride + (r % a.lam_lpp)] = lp;
+        }
+        if (DYK) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) v[k] += pb[k];
+        }
+        st_contig<T, E>(a.out + r * a.stride, i0, n, vec, v);
+    }
+}
+
+// ===========================================================================
 // Column backward: B <- B + colsegmean(A - B)  (Dykstra column adjoint).
 // ===========================================================================
 template <typename T, int E, int LPR, int WPB>

@@ -161,9 +161,28 @@ static cudaError_t row_bwd_t(const RowBwdArgs<T>& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <typename T, int E, int WPL, bool DYK, bool PE>
+static cudaError_t row_bwd_w_t(const RowBwdArgs<T>& a, cudaStream_t s) {
+    auto kern = k_row_bwd_w<T, E, WPL, DYK, PE>;
+    const int grid = persistent_grid(kern, WPL * 32, 0, a.nlines);
+    kern<<<grid, WPL * 32, 0, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
+    if (a.n > 512) {                              // long lines: 4 warps x 8 samples per thread
+        if (dykstra) return row_bwd_w_t<T, 8, 4, true, false>(a, s);
+        if (per_edge) return row_bwd_w_t<T, 8, 4, false, true>(a, s);
+        return row_bwd_w_t<T, 8, 4, false, false>(a, s);
+    }
+    if (a.n > 256) {                              // 2 warps x 8
+        if (dykstra) return row_bwd_w_t<T, 8, 2, true, false>(a, s);
+        if (per_edge) return row_bwd_w_t<T, 8, 2, false, true>(a, s);
+        return row_bwd_w_t<T, 8, 2, false, false>(a, s);
+    }
     TVP_GEO_DISPATCH(a.n, {
         if (dykstra) e = row_bwd_t<T, E_, L_, true, false>(a, s);
         else if (per_edge) e = row_bwd_t<T, E_, L_, false, true>(a, s);

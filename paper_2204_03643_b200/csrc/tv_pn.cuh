@@ -341,16 +341,17 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
 
 // ---------------------------------------------------------------------------
 // Backward primitive: v <- segment-wise mean of v (Eq. 7 under reading O12:
-// the symmetric projector onto vectors constant on the segments).  Segments end
-// at edges in `bnd`; the jump sign of edge k is +1 (pos), -1 (neg) or 0.
-// lam_part += sum over segments ending in this lane of (s_R - s_L) * mean
-// (dx/dlam = (s_R - s_L)/len).
+// the symmetric projector onto vectors constant on the segments), for a line
+// held by a Comm group.  Segments end at edges in `bnd`; the jump sign of edge
+// k is +1 (pos), -1 (neg) or 0.  lam_part += sum_e s_e (mean_left(e) -
+// mean_right(e)) = sum_seg (s_R - s_L) mean_seg (dx/dlam = (s_R - s_L)/len).
+// Comm slots 0..2 are used.
 // ---------------------------------------------------------------------------
-template <typename T, int E, int LPR>
-__device__ __forceinline__ void seg_mean(T (&v)[E], uint32_t bnd, uint32_t pos, uint32_t neg, int l,
-                                         T& lam_part) {
-    // lane pass: lane-local segment sums at segment ends (the first segment of the
-    // lane still lacks the carry) and the open tail
+template <typename T, int E, int LPR, int WPL>
+__device__ __forceinline__ void seg_mean_c(T (&v)[E], uint32_t bnd, uint32_t pos, uint32_t neg,
+                                           const Comm<T, LPR, WPL>& C, T& lam_part) {
+    // pass 1: lane-local segment sums at segment ends (the lane's first segment
+    // still lacks the carry) and the open tail
     T s = T(0), sf = T(0);
     bool hf = false;
 #pragma unroll
@@ -364,42 +365,23 @@ __device__ __forceinline__ void seg_mean(T (&v)[E], uint32_t bnd, uint32_t pos, 
     }
     const int hb = 31 - __clz(bnd);
     const bool fl = bnd != 0u;
-    // carry: (tail sum, tail count) and the sign of the boundary before the tail
     T cs = s;
     int cc = E - 1 - hb;
-    seg_scan_fwd<LPR>(cs, cc, fl, l);
-    const int sl_own = hb < 0 ? 0 : (bit<E>(pos, hb & 31) ? 1 : (bit<E>(neg, hb & 31) ? -1 : 0));
-    // sign of the last boundary left of the lane (nearest flagged lane to the left)
-    int slc = sl_own;
-    bool fs = fl;
-#pragma unroll
-    for (int d = 1; d < LPR; d <<= 1) {
-        int s2 = shup<LPR>((slc + 2) | (fs ? 4 : 0), d);
-        if (l >= d && !fs) { slc = (s2 & 3) - 2; fs = (s2 & 4) != 0; }
-    }
-    int sle = shup<LPR>((slc + 2) | (fs ? 4 : 0), 1);
-    const int csl = (l == 0 || !(sle & 4)) ? 0 : ((sle & 3) - 2);
+    C.template scan_fwd<0>(cs, cc, fl);
     const int fb = __ffs(bnd) - 1;
     const uint32_t firstm = bnd ? ((bnd & (0u - bnd)) * 2u - 1u) : 0u;
     const T fv = (sf + cs) * rcp_(T(fb + 1 + cc));
-    T lp = T(0);
-    int prev_s = csl;
+    // pass 2: means at segment ends
     T cnt = T(0);
-    // means at segment ends and the lambda-gradient terms (s_R - s_L) * mean
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         cnt += T(1);
         const bool bk = bit<E>(bnd, k);
-        const bool isf = bit<E>(firstm, k);
-        const T m = isf ? fv : v[k] * rcp_(cnt);
-        const int sr = bit<E>(pos, k) ? 1 : (bit<E>(neg, k) ? -1 : 0);
-        lp += bk ? T(sr - prev_s) * m : T(0);
-        prev_s = bk ? sr : prev_s;
-        v[k] = bk ? m : v[k];
+        v[k] = bk ? (bit<E>(firstm, k) ? fv : v[k] * rcp_(cnt)) : v[k];
         cnt = bk ? T(0) : cnt;
     }
-    lam_part += lp;
-    T cur = seg_scan_rev<LPR>(fv, fl, l);
+    // pass 3 (reverse): broadcast each segment's mean to its samples
+    T cur = C.template scan_rev<2>(fv, fl);
 #pragma unroll
     for (int k = E - 1; k >= 0; --k) {
         T x = bit<E>(bnd, k) ? v[k] : cur;
@@ -407,6 +389,24 @@ __device__ __forceinline__ void seg_mean(T (&v)[E], uint32_t bnd, uint32_t pos, 
         v[k] = x;
         cur = x;
     }
+    // lambda gradient in edge form
+    const T vn = C.template next<1>(v[0]);
+    T lp = T(0);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const T d = v[k] - ((k + 1 < E) ? v[(k + 1 < E) ? k + 1 : k] : vn);
+        lp += bit<E>(pos, k) ? d : T(0);
+        lp -= bit<E>(neg, k) ? d : T(0);
+    }
+    lam_part += lp;
+}
+
+// Warp-group form (WPL = 1) used by the tiled column / short-row kernels.
+template <typename T, int E, int LPR>
+__device__ __forceinline__ void seg_mean(T (&v)[E], uint32_t bnd, uint32_t pos, uint32_t neg, int l,
+                                         T& lam_part) {
+    const Comm<T, LPR, 1> C{l, 0, nullptr, nullptr};
+    seg_mean_c<T, E, LPR, 1>(v, bnd, pos, neg, C, lam_part);
 }
 
 }  // namespace tvp
