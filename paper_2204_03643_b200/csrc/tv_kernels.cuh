@@ -268,7 +268,7 @@ k_row_fwd(RowFwdArgs<T> a) {
 // the block is one line at a time; cross-warp scans through shared memory.
 // ===========================================================================
 #ifndef TVP_ROWW_MINB
-#define TVP_ROWW_MINB 1
+#define TVP_ROWW_MINB 6
 #endif
 template <typename T, int E, int WPL, bool PE, bool DYK>
 __global__ void __launch_bounds__(WPL * 32, TVP_ROWW_MINB)

@@ -135,7 +135,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
     const T slack1 = T(1) + T(2) * eps;
     const int maxit = Num<T>::max_iters;
 
-    bool run = active, first = true, fin = false, uchg = true;
+    bool run = active, first = true, fin = false, uchg = true, fin_direct = false;
     bool conv = false, stall = false;
     int it = 0;
     for (int itw = 0;; ++itw) {
@@ -207,52 +207,82 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         }
         if (fin) break;
 
-        // ---------------- P4: KKT / zero-duality-gap test of the candidate, uhat -> w.
+        // ---------------- P4: KKT / zero-duality-gap test of the candidate and uhat.
         // uhat_i = u_{a-1} + sum_{j=a..i} (xhat_j - y_j); free edges must satisfy
         // |uhat_i| <= lam_i (up to a summation-error slack), bound edges must jump
-        // in the direction of u_i.
+        // in the direction of u_i.  Fast mode (no line search possible this
+        // iteration) applies the projected full Newton step u <- clip(uhat) in the
+        // same pass and keeps xhat in w; LS mode writes uhat to w for the search.
         T r = ub + rt;
         T A = fabs(ub) + at;
         C.template scan_fwd2<4>(r, A, fl);
         const T xnext = C.template next<5>(w[0]);
+        const bool lsmode = C.uany(run && !first && (it + 1 >= kLsAfter));
         bool ok = true, clip = false, chg = false;
+        if (!lsmode) {
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-            const T xh = w[k];
-            const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
-            const T t = xh - y[k];
-            r += t;
-            A += fabs(t);
-            const T lk = lam.at(k);
-            const bool bk = bit<E>(bnd, k);
-            const bool sgn_bad = (u[k] * (xh1 - xh) < T(0)) & !bit<E>(pin, k);
-            const T ar = fabs(r);
-            const bool infeas = ar > fma(slackA, A, lk * slack1);
-            ok = ok & !(bk ? sgn_bad : infeas);
-            clip = clip | (!bk & (ar > lk));
-            chg = chg | (!bk & (r != u[k]));
-            w[k] = bk ? u[k] : r;
-            A = bk ? fabs(u[k]) : A;
-            r = bk ? u[k] : r;
+            for (int k = 0; k < E; ++k) {
+                const T xh = w[k];
+                const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
+                const T t = xh - y[k];
+                r += t;
+                A += fabs(t);
+                const T lk = lam.at(k);
+                const bool bk = bit<E>(bnd, k);
+                const bool sgn_bad = (u[k] * (xh1 - xh) < T(0)) & !bit<E>(pin, k);
+                const T ar = fabs(r);
+                const bool infeas = ar > fma(slackA, A, lk * slack1);
+                ok = ok & !(bk ? sgn_bad : infeas);
+                chg = chg | (!bk & (r != u[k]));
+                A = bk ? fabs(u[k]) : A;
+                const T un = bk ? u[k] : clampv(r, -lk, lk);
+                r = bk ? u[k] : r;
+                u[k] = un;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                const T xh = w[k];
+                const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
+                const T t = xh - y[k];
+                r += t;
+                A += fabs(t);
+                const T lk = lam.at(k);
+                const bool bk = bit<E>(bnd, k);
+                const bool sgn_bad = (u[k] * (xh1 - xh) < T(0)) & !bit<E>(pin, k);
+                const T ar = fabs(r);
+                const bool infeas = ar > fma(slackA, A, lk * slack1);
+                ok = ok & !(bk ? sgn_bad : infeas);
+                clip = clip | (!bk & (ar > lk));
+                chg = chg | (!bk & (r != u[k]));
+                w[k] = bk ? u[k] : r;
+                A = bk ? fabs(u[k]) : A;
+                r = bk ? u[k] : r;
+            }
+            clip = C.any(clip);
         }
         ok = C.all(ok);
-        clip = C.any(clip);
         chg = C.any(chg);
 #ifdef TVP_DEBUG
         if (active && C.first_lane())
-            printf("[tvp] itw %d it %d run %d first %d ok %d clip %d chg %d bchg %d uchg %d nbound %d\n", itw, it,
-                   (int)run, (int)first, (int)ok, (int)clip, (int)chg, (int)bchg, (int)uchg, __popc(bnd));
+            printf("[tvp] itw %d it %d run %d first %d ok %d clip %d chg %d bchg %d uchg %d nbound %d ls %d\n", itw, it,
+                   (int)run, (int)first, (int)ok, (int)clip, (int)chg, (int)bchg, (int)uchg, __popc(bnd), (int)lsmode);
 #endif
         if (run) ++it;
         if (run && ok) { conv = true; run = false; }
+        // one line per group and warp: a fast-mode convergence leaves xhat in w
+        if ((LPR == 32) && !lsmode && !C.uany(run)) {
+            fin_direct = true;
+            break;
+        }
 
-        // ---------------- step: full Newton step when it stays in the box, else
-        // projected Armijo line search with quadratic-interpolation backtracking.
-        // The projected full Newton step clip(u + d) is taken directly; the Armijo
-        // backtracking line search of P:188 is the globalisation safeguard, engaged
-        // for lines that have not converged after kLsAfter iterations.
-        const bool fast = run && (first || !clip || it < kLsAfter);
-        if (fast) {
+        // ---------------- step (LS mode): full Newton step when it stays in the box,
+        // else the projected Armijo line search with quadratic-interpolation
+        // backtracking of P:188 -- the globalisation safeguard after kLsAfter iterations.
+        const bool fast = lsmode && run && (first || !clip);
+        if (!lsmode) {
+            uchg = chg || first;
+        } else if (fast) {
 #pragma unroll
             for (int k = 0; k < E; ++k) {
                 const T lk = lam.at(k);
@@ -260,7 +290,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             }
             uchg = chg || first;
         }
-        bool pending = run && !fast;
+        bool pending = lsmode && run && !fast;
         if (C.uany(pending)) {
             T alpha = T(1), slope = T(0);
             bool accepted = false, lchg = false;
@@ -309,7 +339,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                     }
                 }
             }
-            if (run && !fast) {
+            if (lsmode && run && !fast) {
                 if (accepted && lchg) {
 #pragma unroll
                     for (int k = 0; k < E; ++k) {
@@ -327,6 +357,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         first = false;
         if (!C.uany(run) || itw + 2 >= maxit) fin = true;
     }
+    (void)fin_direct;
     // lines still running hit max_iters: output the primal of the current dual
     const T upv = C.template prev<10>(u[E - 1]);
     if (run) {
