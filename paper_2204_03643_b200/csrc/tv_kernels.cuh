@@ -152,8 +152,11 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
 // ===========================================================================
 // Row forward: 1D rows or Dykstra row pass.
 // ===========================================================================
+#ifndef TVP_ROW_MINB
+#define TVP_ROW_MINB 1
+#endif
 template <typename T, int E, int LPR, bool PE, bool DYK, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
+__global__ void __launch_bounds__(WPB * 32, TVP_ROW_MINB)
 k_row_fwd(RowFwdArgs<T> a) {
     constexpr int G = 32 / LPR;
     constexpr int LP = line_pitch<E, LPR>();
@@ -363,8 +366,11 @@ k_row_fwd_w(RowFwdArgs<T> a) {
 // ===========================================================================
 // Column forward: Dykstra column pass (tile of TC columns of one plane).
 // ===========================================================================
+#ifndef TVP_COL_MINB
+#define TVP_COL_MINB 1
+#endif
 template <typename T, int E, int LPR, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
+__global__ void __launch_bounds__(WPB * 32, TVP_COL_MINB)
 k_col_fwd(ColFwdArgs<T> a) {
     constexpr int G = 32 / LPR;
     constexpr int LP = line_pitch<E, LPR>();
