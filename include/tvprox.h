@@ -165,6 +165,37 @@ tvp_status_t tv2d_prox_bwd(tvp_dtype_t dt, const void *grad_Y, const void *saved
                            tvp_lam_mode_t lm, int iters, void *workspace,
                            tvp_stream_t stream);
 
+/* ----------------------------------------------------- TV layer (NEXT f1) --- */
+/*
+ * The TV layer of Sec. 3.1 (Eq. 3-4, Fig. 2) is built from the calls
+ * above plus these.  Rows-only / columns-only spatial modes ("a 1D
+ * TV-proximity operator per row or column"): one 1D prox per image row
+ * (axis 0, lines of W samples) or image column (axis 1, lines of H samples) of
+ * every plane of a contiguous NCHW tensor; lam per TVP_LAM_SCALAR,
+ * TVP_LAM_PER_CHANNEL or TVP_LAM_PER_PLANE.  mask (nullable, needed by the
+ * bwd): axis 0 [N*C][H][ceil((W-1)/16)], axis 1 [N*C][W][ceil((H-1)/16)].
+ */
+tvp_status_t tv2d_lines_fwd(tvp_dtype_t dt, const void *X, void *Y,
+                            int64_t N, int64_t C, int64_t H, int64_t W,
+                            const void *lam, tvp_lam_mode_t lm, double lam_scalar, int axis,
+                            uint32_t *mask, tvp_stream_t stream);
+size_t tv2d_lines_workspace_bytes(tvp_dtype_t dt, int64_t N, int64_t C, int64_t H, int64_t W, int axis);
+tvp_status_t tv2d_lines_bwd(tvp_dtype_t dt, const void *grad_Y, const uint32_t *mask, void *grad_X,
+                            void *grad_lam, int64_t N, int64_t C, int64_t H, int64_t W,
+                            tvp_lam_mode_t lm, int axis, void *workspace, tvp_stream_t stream);
+
+/* lam = SoftPlus(t) = log(1 + e^t), elementwise over n values (Eq. 3). */
+tvp_status_t tvp_softplus_fwd(tvp_dtype_t dt, const void *t, void *lam, int64_t n, tvp_stream_t stream);
+/* grad_t = grad_lam * sigmoid(t) (the derivative of SoftPlus). */
+tvp_status_t tvp_softplus_bwd(tvp_dtype_t dt, const void *t, const void *grad_lam, void *grad_t,
+                              int64_t n, tvp_stream_t stream);
+/* y = a*x + b*y over n values (x may be NULL when a == 0; y is not read when
+ * b == 0).  Sharpening mode
+ * (Eq. 4): Y = 2X - prox(X) is axpby(X, Y_prox, 2, -1); its VJP
+ * grad_X = 2G - VJP(G) is axpby(G, VJP(G), 2, -1) and grad_lam is negated. */
+tvp_status_t tvp_axpby(tvp_dtype_t dt, const void *x, void *y, double a, double b, int64_t n,
+                       tvp_stream_t stream);
+
 /* ------------------------------------------------------------ utilities --- */
 const char *tvp_status_string(tvp_status_t s);
 const char *tvp_last_error(void);          /* last TVP_ECUDA / TVP_EINVAL message (thread-local) */

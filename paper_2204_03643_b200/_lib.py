@@ -22,6 +22,8 @@ EXPORTS = [
     "tvp_max_line", "tv1d_mask_words", "tv1d_prox_fwd", "tv1d_prox_fwd_warm", "tv1d_bwd_workspace_bytes",
     "tv1d_prox_bwd",
     "tv2d_saved_bytes", "tv2d_workspace_bytes", "tv2d_prox_fwd", "tv2d_prox_bwd",
+    "tv2d_lines_fwd", "tv2d_lines_workspace_bytes", "tv2d_lines_bwd",
+    "tvp_softplus_fwd", "tvp_softplus_bwd", "tvp_axpby",
     "tvp_status_string", "tvp_last_error", "tvp_version", "tvp_launch_count",
 ]
 
@@ -66,6 +68,18 @@ def load(path: str = LIB_PATH):
         lib.tv2d_prox_fwd.restype = i32
         lib.tv2d_prox_bwd.argtypes = [i32, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, vp, vp]
         lib.tv2d_prox_bwd.restype = i32
+        lib.tv2d_lines_fwd.argtypes = [i32, vp, vp, i64, i64, i64, i64, vp, i32, dbl, i32, vp, vp]
+        lib.tv2d_lines_fwd.restype = i32
+        lib.tv2d_lines_workspace_bytes.argtypes = [i32, i64, i64, i64, i64, i32]
+        lib.tv2d_lines_workspace_bytes.restype = u64
+        lib.tv2d_lines_bwd.argtypes = [i32, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, vp, vp]
+        lib.tv2d_lines_bwd.restype = i32
+        lib.tvp_softplus_fwd.argtypes = [i32, vp, vp, i64, vp]
+        lib.tvp_softplus_fwd.restype = i32
+        lib.tvp_softplus_bwd.argtypes = [i32, vp, vp, vp, i64, vp]
+        lib.tvp_softplus_bwd.restype = i32
+        lib.tvp_axpby.argtypes = [i32, vp, vp, dbl, dbl, i64, vp]
+        lib.tvp_axpby.restype = i32
         lib.tvp_status_string.argtypes = [i32]
         lib.tvp_status_string.restype = ctypes.c_char_p
         lib.tvp_last_error.argtypes = []

@@ -803,4 +803,31 @@ __global__ void __launch_bounds__(256) k_lam_reduce2(LamReduceArgs<T> a) {
     }
 }
 
+// ===========================================================================
+// Elementwise helpers of the TV layer (Eq. 3-4): SoftPlus, its derivative, axpby.
+// ===========================================================================
+template <typename T>
+__global__ void k_softplus_fwd(const T* __restrict__ t, T* __restrict__ lam, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = t[i];
+        lam[i] = (v > T(0) ? v : T(0)) + log1p(exp(-fabs(v)));
+    }
+}
+template <typename T>
+__global__ void k_softplus_bwd(const T* __restrict__ t, const T* __restrict__ g, T* __restrict__ gt, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = t[i];
+        const T e = exp(-fabs(v));
+        const T sig = v >= T(0) ? T(1) / (T(1) + e) : e / (T(1) + e);
+        gt[i] = g[i] * sig;
+    }
+}
+template <typename T>
+__global__ void k_axpby(const T* __restrict__ x, T* __restrict__ y, T a, T b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T xv = x ? x[i] : T(0);
+        y[i] = (b != T(0)) ? a * xv + b * y[i] : a * xv;   // b == 0: y is write-only
+    }
+}
+
 }  // namespace tvp

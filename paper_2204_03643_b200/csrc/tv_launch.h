@@ -42,6 +42,9 @@ template <typename T> cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dy
 template <typename T> cudaError_t launch_col_bwd(ColBwdArgs<T> a, cudaStream_t s);
 template <typename T> cudaError_t launch_lam_reduce(const LamReduceArgs<T>& a, cudaStream_t s);
 
+template <typename T> cudaError_t launch_softplus(const T* t, T* lam, const T* g, T* gt, int64_t n, bool bwd, cudaStream_t s);
+template <typename T> cudaError_t launch_axpby(const T* x, T* y, T a, T b, int64_t n, cudaStream_t s);
+
 void count_launch();
 
 }  // namespace tvp

@@ -224,11 +224,33 @@ cudaError_t launch_lam_reduce(const LamReduceArgs<T>& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+static int elementwise_grid(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+template <typename T>
+cudaError_t launch_softplus(const T* t, T* lam, const T* g, T* gt, int64_t n, bool bwd, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (bwd) k_softplus_bwd<T><<<elementwise_grid(n), 256, 0, s>>>(t, g, gt, n);
+    else k_softplus_fwd<T><<<elementwise_grid(n), 256, 0, s>>>(t, lam, n);
+    count_launch();
+    return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_axpby(const T* x, T* y, T a, T b, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_axpby<T><<<elementwise_grid(n), 256, 0, s>>>(x, y, a, b, n);
+    count_launch();
+    return cudaGetLastError();
+}
+
 #define TVP_INSTANTIATE(T)                                                                         \
     template cudaError_t launch_row_fwd<T>(const RowFwdArgs<T>&, bool, bool, cudaStream_t);        \
     template cudaError_t launch_col_fwd<T>(ColFwdArgs<T>, cudaStream_t);                           \
     template cudaError_t launch_row_bwd<T>(const RowBwdArgs<T>&, bool, bool, cudaStream_t);        \
     template cudaError_t launch_col_bwd<T>(ColBwdArgs<T>, cudaStream_t);                           \
-    template cudaError_t launch_lam_reduce<T>(const LamReduceArgs<T>&, cudaStream_t);
+    template cudaError_t launch_lam_reduce<T>(const LamReduceArgs<T>&, cudaStream_t);                \
+    template cudaError_t launch_softplus<T>(const T*, T*, const T*, T*, int64_t, bool, cudaStream_t);\
+    template cudaError_t launch_axpby<T>(const T*, T*, T, T, int64_t, cudaStream_t);
 
 }  // namespace tvp

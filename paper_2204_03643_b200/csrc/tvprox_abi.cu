@@ -394,3 +394,168 @@ extern "C" tvp_status_t tv2d_prox_bwd(tvp_dtype_t dt, const void* grad_Y, const 
     return dt == TVP_F32 ? tv2d_bwd_impl<float>(grad_Y, saved, grad_X, grad_lam, N, C, H, W, lm, iters, workspace, s)
                          : tv2d_bwd_impl<double>(grad_Y, saved, grad_X, grad_lam, N, C, H, W, lm, iters, workspace, s);
 }
+
+// ------------------------------------------------------------ TV layer (f1)
+static bool lines_args_ok(int64_t N, int64_t C, int64_t H, int64_t W, int axis) {
+    return N >= 0 && C >= 0 && H >= 1 && W >= 1 && (axis == 0 || axis == 1);
+}
+
+extern "C" size_t tv2d_lines_workspace_bytes(tvp_dtype_t dt, int64_t N, int64_t C, int64_t H, int64_t W, int axis) {
+    if (!lines_args_ok(N, C, H, W, axis)) return 0;
+    const size_t esz = dt == TVP_F64 ? 8 : 4;
+    const int64_t planes = N * C;
+    const int64_t lines = planes * (axis == 0 ? H : W);
+    return align256((size_t)lines * esz) + align256((size_t)512 * (planes > 0 ? planes : 1) * esz);
+}
+
+template <typename T>
+static tvp_status_t lines_fwd_impl(const void* X, void* Y, int64_t N, int64_t C, int64_t H, int64_t W,
+                                   const void* lam, tvp_lam_mode_t lm, double lam_scalar, int axis, uint32_t* mask,
+                                   cudaStream_t s) {
+    const int64_t planes = N * C;
+    if (axis == 0) {
+        RowFwdArgs<T> a{};
+        a.src0 = static_cast<const T*>(X);
+        a.dst0 = static_cast<T*>(Y);
+        a.lam = static_cast<const T*>(lam);
+        a.lam_mode = (int)lm;
+        a.lam_scalar = (T)lam_scalar;
+        a.nlines = planes * H;
+        a.n = (int)W;
+        a.stride = W;
+        a.lines_per_plane = H;
+        a.C = (int)(C > 0 ? C : 1);
+        a.mask_out = mask;
+        a.mw = (int)mask_words(W);
+        return cuda_status(launch_row_fwd<T>(a, false, false, s), "tv2d_lines_fwd(rows)");
+    }
+    ColFwdArgs<T> c{};
+    c.Z = static_cast<const T*>(X);
+    c.Y = static_cast<T*>(Y);
+    c.lam = static_cast<const T*>(lam);
+    c.lam_mode = (int)lm;
+    c.lam_scalar = (T)lam_scalar;
+    c.C = (int)(C > 0 ? C : 1);
+    c.planes = planes;
+    c.H = (int)H;
+    c.W = (int)W;
+    c.mask_out = mask;
+    c.mw = (int)mask_words(H);
+    return cuda_status(launch_col_fwd<T>(c, s), "tv2d_lines_fwd(cols)");
+}
+
+extern "C" tvp_status_t tv2d_lines_fwd(tvp_dtype_t dt, const void* X, void* Y, int64_t N, int64_t C, int64_t H,
+                                       int64_t W, const void* lam, tvp_lam_mode_t lm, double lam_scalar, int axis,
+                                       uint32_t* mask, tvp_stream_t stream) {
+    if (dt != TVP_F32 && dt != TVP_F64) return fail(TVP_EINVAL, "tv2d_lines_fwd: bad dtype");
+    if (!lines_args_ok(N, C, H, W, axis)) return fail(TVP_EINVAL, "tv2d_lines_fwd: need N, C >= 0, H, W >= 1, axis 0/1");
+    if (!lam2d_ok(lm, lam, lam_scalar)) return fail(TVP_EINVAL, "tv2d_lines_fwd: invalid lam / lam mode");
+    if (N * C == 0) return TVP_OK;
+    if (!X || !Y) return fail(TVP_EINVAL, "tv2d_lines_fwd: NULL X or Y");
+    if ((axis == 0 ? W : H) > kMaxLine) return fail(TVP_EUNSUPPORTED, "tv2d_lines_fwd: line > tvp_max_line()");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    return dt == TVP_F32 ? lines_fwd_impl<float>(X, Y, N, C, H, W, lam, lm, lam_scalar, axis, mask, s)
+                         : lines_fwd_impl<double>(X, Y, N, C, H, W, lam, lm, lam_scalar, axis, mask, s);
+}
+
+template <typename T>
+static tvp_status_t lines_bwd_impl(const void* G, const uint32_t* mask, void* GX, void* glam, int64_t N, int64_t C,
+                                   int64_t H, int64_t W, tvp_lam_mode_t lm, int axis, void* ws, cudaStream_t s) {
+    const int64_t planes = N * C;
+    const int64_t L = axis == 0 ? H : W;            // lines per plane
+    T* part = static_cast<T*>(ws);
+    cudaError_t e;
+    if (axis == 0) {
+        RowBwdArgs<T> r{};
+        r.A = static_cast<const T*>(G);
+        r.out = static_cast<T*>(GX);
+        r.mask = mask;
+        r.mw = (int)mask_words(W);
+        r.nlines = planes * H;
+        r.n = (int)W;
+        r.stride = W;
+        r.lam_line = glam ? part : nullptr;
+        r.lam_lpp = 1;
+        r.lam_pstride = 1;
+        e = launch_row_bwd<T>(r, false, false, s);
+    } else {
+        ColBwdArgs<T> c{};
+        c.A = static_cast<const T*>(G);
+        c.B = nullptr;
+        c.Bout = static_cast<T*>(GX);
+        c.mask = mask;
+        c.mw = (int)mask_words(H);
+        c.planes = planes;
+        c.H = (int)H;
+        c.W = (int)W;
+        c.lam_line = glam ? part : nullptr;
+        c.lam_pstride = W;
+        e = launch_col_bwd<T>(c, s);
+    }
+    if (e != cudaSuccess) return cuda_status(e, "tv2d_lines_bwd");
+    if (glam) {
+        LamReduceArgs<T> q{};
+        q.part = part;
+        q.out = static_cast<T*>(glam);
+        if (lm == TVP_LAM_SCALAR) {
+            q.nout = 1; q.reps = 1; q.rep_stride = 0; q.q_stride = 0; q.seglen = planes * L;
+        } else if (lm == TVP_LAM_PER_CHANNEL) {
+            q.nout = C; q.reps = N; q.rep_stride = C * L; q.q_stride = L; q.seglen = L;
+        } else {
+            q.nout = planes; q.reps = 1; q.rep_stride = 0; q.q_stride = L; q.seglen = L;
+        }
+        q.nchunk = lam_chunks(q.reps * q.seglen, q.nout);
+        q.scratch = reinterpret_cast<T*>(static_cast<char*>(ws) + align256((size_t)planes * L * sizeof(T)));
+        e = launch_lam_reduce<T>(q, s);
+    }
+    return cuda_status(e, "tv2d_lines_bwd(lam)");
+}
+
+extern "C" tvp_status_t tv2d_lines_bwd(tvp_dtype_t dt, const void* grad_Y, const uint32_t* mask, void* grad_X,
+                                       void* grad_lam, int64_t N, int64_t C, int64_t H, int64_t W,
+                                       tvp_lam_mode_t lm, int axis, void* workspace, tvp_stream_t stream) {
+    if (dt != TVP_F32 && dt != TVP_F64) return fail(TVP_EINVAL, "tv2d_lines_bwd: bad dtype");
+    if (!lines_args_ok(N, C, H, W, axis)) return fail(TVP_EINVAL, "tv2d_lines_bwd: need N, C >= 0, H, W >= 1, axis 0/1");
+    if (lm != TVP_LAM_SCALAR && lm != TVP_LAM_PER_CHANNEL && lm != TVP_LAM_PER_PLANE)
+        return fail(TVP_EINVAL, "tv2d_lines_bwd: lam mode must be SCALAR, PER_CHANNEL or PER_PLANE");
+    if (N * C == 0) return TVP_OK;
+    const int64_t L = axis == 0 ? W : H;
+    if (!grad_Y || !grad_X || (L > 1 && !mask)) return fail(TVP_EINVAL, "tv2d_lines_bwd: NULL grad_Y, grad_X or mask");
+    if (grad_lam && !workspace) return fail(TVP_EINVAL, "tv2d_lines_bwd: NULL workspace");
+    if (L > kMaxLine) return fail(TVP_EUNSUPPORTED, "tv2d_lines_bwd: line > tvp_max_line()");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    return dt == TVP_F32 ? lines_bwd_impl<float>(grad_Y, mask, grad_X, grad_lam, N, C, H, W, lm, axis, workspace, s)
+                         : lines_bwd_impl<double>(grad_Y, mask, grad_X, grad_lam, N, C, H, W, lm, axis, workspace, s);
+}
+
+extern "C" tvp_status_t tvp_softplus_fwd(tvp_dtype_t dt, const void* t, void* lam, int64_t n, tvp_stream_t stream) {
+    if ((dt != TVP_F32 && dt != TVP_F64) || n < 0) return fail(TVP_EINVAL, "tvp_softplus_fwd: bad arguments");
+    if (n == 0) return TVP_OK;
+    if (!t || !lam) return fail(TVP_EINVAL, "tvp_softplus_fwd: NULL pointer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = dt == TVP_F32 ? launch_softplus<float>((const float*)t, (float*)lam, nullptr, nullptr, n, false, s)
+                                  : launch_softplus<double>((const double*)t, (double*)lam, nullptr, nullptr, n, false, s);
+    return cuda_status(e, "tvp_softplus_fwd");
+}
+
+extern "C" tvp_status_t tvp_softplus_bwd(tvp_dtype_t dt, const void* t, const void* g, void* gt, int64_t n,
+                                         tvp_stream_t stream) {
+    if ((dt != TVP_F32 && dt != TVP_F64) || n < 0) return fail(TVP_EINVAL, "tvp_softplus_bwd: bad arguments");
+    if (n == 0) return TVP_OK;
+    if (!t || !g || !gt) return fail(TVP_EINVAL, "tvp_softplus_bwd: NULL pointer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = dt == TVP_F32 ? launch_softplus<float>((const float*)t, nullptr, (const float*)g, (float*)gt, n, true, s)
+                                  : launch_softplus<double>((const double*)t, nullptr, (const double*)g, (double*)gt, n, true, s);
+    return cuda_status(e, "tvp_softplus_bwd");
+}
+
+extern "C" tvp_status_t tvp_axpby(tvp_dtype_t dt, const void* x, void* y, double a, double b, int64_t n,
+                                  tvp_stream_t stream) {
+    if ((dt != TVP_F32 && dt != TVP_F64) || n < 0) return fail(TVP_EINVAL, "tvp_axpby: bad arguments");
+    if (n == 0) return TVP_OK;
+    if (!y || (!x && a != 0.0)) return fail(TVP_EINVAL, "tvp_axpby: NULL pointer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = dt == TVP_F32 ? launch_axpby<float>((const float*)x, (float*)y, (float)a, (float)b, n, s)
+                                  : launch_axpby<double>((const double*)x, (double*)y, a, b, n, s);
+    return cuda_status(e, "tvp_axpby");
+}

@@ -236,6 +236,100 @@ def tv2d(X: torch.Tensor, lam, iters: int = 4) -> torch.Tensor:
     return TV2DProx.apply(X, None, float(lam), int(iters))
 
 
+# --------------------------------------------------- TV layer pieces (NEXT f1)
+def tv2d_lines_fwd(X: torch.Tensor, lam, axis: int, need_mask: bool = True):
+    """Rows-only (axis 0) / columns-only (axis 1) spatial mode.  Returns (Y, mask)."""
+    _require_cuda(X)
+    X = X.contiguous()
+    dt = _dtype_code(X)
+    lib = _lib.load()
+    N, C, H, W = X.shape
+    mode, scal, lt = _lam2d(lam, X)
+    Y = torch.empty_like(X)
+    L, n = (H, W) if axis == 0 else (W, H)
+    mask = None
+    if need_mask:
+        mw = lib.tv1d_mask_words(n)
+        mask = torch.empty((N * C * L, max(mw, 1)), device=X.device, dtype=torch.int32)
+    check(lib.tv2d_lines_fwd(dt, _ptr(X), _ptr(Y), N, C, H, W, _ptr(lt), mode, scal, int(axis), _ptr(mask),
+                             _stream(X)), "tv2d_lines_fwd")
+    return Y, mask
+
+
+def tv2d_lines_bwd(grad_Y: torch.Tensor, mask: torch.Tensor, lam_mode: int, axis: int, want_lam: bool = True):
+    _require_cuda(grad_Y, mask)
+    G = grad_Y.contiguous()
+    dt = _dtype_code(G)
+    lib = _lib.load()
+    N, C, H, W = G.shape
+    GX = torch.empty_like(G)
+    glam = None
+    if want_lam:
+        cnt = {_lib.LAM_SCALAR: 1, _lib.LAM_PER_CHANNEL: C, _lib.LAM_PER_PLANE: N * C}[lam_mode]
+        glam = torch.empty(max(cnt, 1), device=G.device, dtype=G.dtype)
+    ws = torch.empty(max(lib.tv2d_lines_workspace_bytes(dt, N, C, H, W, int(axis)), 1), device=G.device,
+                     dtype=torch.uint8)
+    check(lib.tv2d_lines_bwd(dt, _ptr(G), _ptr(mask), _ptr(GX), _ptr(glam), N, C, H, W, lam_mode, int(axis),
+                             _ptr(ws), _stream(G)), "tv2d_lines_bwd")
+    return GX, glam
+
+
+class TVLinesProx(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, X, lam_t, lam_scalar, axis):
+        lam = lam_scalar if lam_t is None else lam_t
+        Y, mask = tv2d_lines_fwd(X, lam, axis)
+        mode, _, _ = _lam2d(lam, X)
+        ctx.save_for_backward(mask)
+        ctx.mode, ctx.axis = mode, axis
+        ctx.lam_shape = None if lam_t is None else lam_t.shape
+        return Y
+
+    @staticmethod
+    def backward(ctx, gY):
+        (mask,) = ctx.saved_tensors
+        need_lam = ctx.needs_input_grad[1]
+        gX, gl = tv2d_lines_bwd(gY, mask, ctx.mode, ctx.axis, want_lam=need_lam)
+        if need_lam and gl is not None and ctx.lam_shape is not None:
+            gl = gl.reshape(ctx.lam_shape)
+        return gX, (gl if need_lam else None), None, None
+
+
+def tv2d_lines(X: torch.Tensor, lam, axis: int) -> torch.Tensor:
+    if torch.is_tensor(lam):
+        return TVLinesProx.apply(X, lam, 0.0, int(axis))
+    return TVLinesProx.apply(X, None, float(lam), int(axis))
+
+
+def softplus_fwd(t: torch.Tensor) -> torch.Tensor:
+    _require_cuda(t)
+    t = t.contiguous()
+    out = torch.empty_like(t)
+    check(_lib.load().tvp_softplus_fwd(_dtype_code(t), _ptr(t), _ptr(out), t.numel(), _stream(t)), "tvp_softplus_fwd")
+    return out
+
+
+def softplus_bwd(t: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
+    _require_cuda(t, g)
+    t, g = t.contiguous(), g.contiguous().to(t.dtype)
+    out = torch.empty_like(t)
+    check(_lib.load().tvp_softplus_bwd(_dtype_code(t), _ptr(t), _ptr(g), _ptr(out), t.numel(), _stream(t)),
+          "tvp_softplus_bwd")
+    return out
+
+
+def axpby_(x, y: torch.Tensor, a: float, b: float) -> torch.Tensor:
+    """In place: y <- a x + b y (one kernel)."""
+    _require_cuda(y)
+    if x is not None:
+        _require_cuda(x)
+        x = x.contiguous()
+    assert y.is_contiguous()
+    check(_lib.load().tvp_axpby(_dtype_code(y), _ptr(x), _ptr(y), float(a), float(b), y.numel(), _stream(y)),
+          "tvp_axpby")
+    return y
+
+
 def unpack_mask(mask: torch.Tensor, n: int) -> torch.Tensor:
     """[lines, words] int32 -> [lines, n-1] uint8 2-bit codes (host-side helper for tests/diagnostics)."""
     m = mask.to(torch.int64) & 0xFFFFFFFF
