@@ -35,6 +35,13 @@ class TVProxError(RuntimeError):
     pass
 
 
+def _sig(lib, name, attr, value):
+    """Type one entry point (an older library build lacking it is tolerated; calling it raises)."""
+    fn = getattr(lib, name, None)
+    if fn is not None:
+        setattr(fn, attr, value)
+
+
 def load(path: str = LIB_PATH):
     """Load and type the library (once)."""
     global _lib
@@ -48,46 +55,46 @@ def load(path: str = LIB_PATH):
         lib = ctypes.CDLL(path)
         i64, i32, u64 = ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
         vp, dbl = ctypes.c_void_p, ctypes.c_double
-        lib.tvp_max_line.argtypes = [i32]
-        lib.tvp_max_line.restype = i64
-        lib.tv1d_mask_words.argtypes = [i64]
-        lib.tv1d_mask_words.restype = u64
-        lib.tv1d_prox_fwd.argtypes = [i32, vp, vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp]
-        lib.tv1d_prox_fwd.restype = i32
-        lib.tv1d_prox_fwd_warm.argtypes = [i32, vp, vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp, vp]
-        lib.tv1d_prox_fwd_warm.restype = i32
-        lib.tv1d_bwd_workspace_bytes.argtypes = [i32, i64, i32]
-        lib.tv1d_bwd_workspace_bytes.restype = u64
-        lib.tv1d_prox_bwd.argtypes = [i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, vp]
-        lib.tv1d_prox_bwd.restype = i32
-        lib.tv2d_saved_bytes.argtypes = [i64, i64, i64, i64, i32]
-        lib.tv2d_saved_bytes.restype = u64
-        lib.tv2d_workspace_bytes.argtypes = [i32, i64, i64, i64, i64, i32]
-        lib.tv2d_workspace_bytes.restype = u64
-        lib.tv2d_prox_fwd.argtypes = [i32, vp, vp, i64, i64, i64, i64, vp, i32, dbl, i32, vp, vp, vp, vp]
-        lib.tv2d_prox_fwd.restype = i32
-        lib.tv2d_prox_bwd.argtypes = [i32, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, vp, vp]
-        lib.tv2d_prox_bwd.restype = i32
-        lib.tv2d_lines_fwd.argtypes = [i32, vp, vp, i64, i64, i64, i64, vp, i32, dbl, i32, vp, vp]
-        lib.tv2d_lines_fwd.restype = i32
-        lib.tv2d_lines_workspace_bytes.argtypes = [i32, i64, i64, i64, i64, i32]
-        lib.tv2d_lines_workspace_bytes.restype = u64
-        lib.tv2d_lines_bwd.argtypes = [i32, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, vp, vp]
-        lib.tv2d_lines_bwd.restype = i32
-        lib.tvp_softplus_fwd.argtypes = [i32, vp, vp, i64, vp]
-        lib.tvp_softplus_fwd.restype = i32
-        lib.tvp_softplus_bwd.argtypes = [i32, vp, vp, vp, i64, vp]
-        lib.tvp_softplus_bwd.restype = i32
-        lib.tvp_axpby.argtypes = [i32, vp, vp, dbl, dbl, i64, vp]
-        lib.tvp_axpby.restype = i32
-        lib.tvp_status_string.argtypes = [i32]
-        lib.tvp_status_string.restype = ctypes.c_char_p
-        lib.tvp_last_error.argtypes = []
-        lib.tvp_last_error.restype = ctypes.c_char_p
-        lib.tvp_version.argtypes = []
-        lib.tvp_version.restype = i32
-        lib.tvp_launch_count.argtypes = [i32]
-        lib.tvp_launch_count.restype = i64
+        _sig(lib, "tvp_max_line", "argtypes", [i32])
+        _sig(lib, "tvp_max_line", "restype", i64)
+        _sig(lib, "tv1d_mask_words", "argtypes", [i64])
+        _sig(lib, "tv1d_mask_words", "restype", u64)
+        _sig(lib, "tv1d_prox_fwd", "argtypes", [i32, vp, vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp])
+        _sig(lib, "tv1d_prox_fwd", "restype", i32)
+        _sig(lib, "tv1d_prox_fwd_warm", "argtypes", [i32, vp, vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp, vp])
+        _sig(lib, "tv1d_prox_fwd_warm", "restype", i32)
+        _sig(lib, "tv1d_bwd_workspace_bytes", "argtypes", [i32, i64, i32])
+        _sig(lib, "tv1d_bwd_workspace_bytes", "restype", u64)
+        _sig(lib, "tv1d_prox_bwd", "argtypes", [i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, vp])
+        _sig(lib, "tv1d_prox_bwd", "restype", i32)
+        _sig(lib, "tv2d_saved_bytes", "argtypes", [i64, i64, i64, i64, i32])
+        _sig(lib, "tv2d_saved_bytes", "restype", u64)
+        _sig(lib, "tv2d_workspace_bytes", "argtypes", [i32, i64, i64, i64, i64, i32])
+        _sig(lib, "tv2d_workspace_bytes", "restype", u64)
+        _sig(lib, "tv2d_prox_fwd", "argtypes", [i32, vp, vp, i64, i64, i64, i64, vp, i32, dbl, i32, vp, vp, vp, vp])
+        _sig(lib, "tv2d_prox_fwd", "restype", i32)
+        _sig(lib, "tv2d_prox_bwd", "argtypes", [i32, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, vp, vp])
+        _sig(lib, "tv2d_prox_bwd", "restype", i32)
+        _sig(lib, "tv2d_lines_fwd", "argtypes", [i32, vp, vp, i64, i64, i64, i64, vp, i32, dbl, i32, vp, vp])
+        _sig(lib, "tv2d_lines_fwd", "restype", i32)
+        _sig(lib, "tv2d_lines_workspace_bytes", "argtypes", [i32, i64, i64, i64, i64, i32])
+        _sig(lib, "tv2d_lines_workspace_bytes", "restype", u64)
+        _sig(lib, "tv2d_lines_bwd", "argtypes", [i32, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, vp, vp])
+        _sig(lib, "tv2d_lines_bwd", "restype", i32)
+        _sig(lib, "tvp_softplus_fwd", "argtypes", [i32, vp, vp, i64, vp])
+        _sig(lib, "tvp_softplus_fwd", "restype", i32)
+        _sig(lib, "tvp_softplus_bwd", "argtypes", [i32, vp, vp, vp, i64, vp])
+        _sig(lib, "tvp_softplus_bwd", "restype", i32)
+        _sig(lib, "tvp_axpby", "argtypes", [i32, vp, vp, dbl, dbl, i64, vp])
+        _sig(lib, "tvp_axpby", "restype", i32)
+        _sig(lib, "tvp_status_string", "argtypes", [i32])
+        _sig(lib, "tvp_status_string", "restype", ctypes.c_char_p)
+        _sig(lib, "tvp_last_error", "argtypes", [])
+        _sig(lib, "tvp_last_error", "restype", ctypes.c_char_p)
+        _sig(lib, "tvp_version", "argtypes", [])
+        _sig(lib, "tvp_version", "restype", i32)
+        _sig(lib, "tvp_launch_count", "argtypes", [i32])
+        _sig(lib, "tvp_launch_count", "restype", i64)
         _lib = lib
         return lib
 

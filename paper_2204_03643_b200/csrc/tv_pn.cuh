@@ -42,7 +42,7 @@ struct Lam {
     __device__ __forceinline__ T at(int k) const { return PE ? e[PE ? k : 0] : r; }
 };
 
-template <int E> __device__ __forceinline__ bool bit(uint32_t m, int k) { return (m >> k) & 1u; }
+template <int E> __device__ __forceinline__ bool bit(uint32_t m, int k) { return (m & (1u << k)) != 0u; }
 
 // Highest set bit of m below position k, or -1.
 __device__ __forceinline__ int prev_bit(uint32_t m, int k) {
@@ -147,26 +147,34 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         const uint32_t keep = upd ? pin : bnd;
         T uprev, unext;
         C.template prev_next<0>(u[E - 1], u[0], uprev, unext);
-        uint32_t nb = 0;
+        // (a) outward-gradient bits at the bound (predicate -> one OR per sample)
+        uint32_t outb = 0;
+        {
+            T xk = y[0] + u[0] - uprev;
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                const T thr = upd ? lam.at(k) : big_<T>();
+                const T xk1 = (k + 1 < E) ? (y[(k + 1 < E) ? k + 1 : k] + u[(k + 1 < E) ? k + 1 : k] - u[k])
+                                          : (ynext + unext - u[k]);
+                const T g = xk1 - xk;
+                xk = xk1;
+                if ((fabs(u[k]) >= thr) & (u[k] * g > T(0))) outb |= 1u << k;
+            }
+        }
+        const uint32_t nb = keep | outb;
+        const uint32_t firstb = nb & (0u - nb);         // lowest bound edge of the lane
+        // (b) lane-local segment numerators / values with the final bits
         T s = T(0), cnt = T(0), numf = T(0), ub = T(0);
-        bool hf = false;
-        T xk = y[0] + u[0] - uprev;
 #pragma unroll
         for (int k = 0; k < E; ++k) {
-            const T thr = upd ? lam.at(k) : big_<T>();
-            const T xk1 = (k + 1 < E) ? (y[(k + 1 < E) ? k + 1 : k] + u[(k + 1 < E) ? k + 1 : k] - u[k])
-                                      : (ynext + unext - u[k]);
-            const T g = xk1 - xk;
-            xk = xk1;
-            const bool bk = bit<E>(keep, k) | ((fabs(u[k]) >= thr) & (u[k] * g > T(0)));
-            nb |= (uint32_t)bk << k;
             s += y[k];
             cnt += T(1);
             const T num = s + u[k];
-            const T val = num * rcp_(cnt);
-            numf = (bk & !hf) ? num : numf;
-            w[k] = bk ? (hf ? val : num) : w[k];
-            hf = hf | bk;
+            const bool bk = bit<E>(nb, k);
+            const bool fk = bit<E>(firstb, k);
+            const T val = fk ? num : num * rcp_(cnt);
+            numf = fk ? num : numf;
+            w[k] = bk ? val : w[k];
             ub = bk ? u[k] : ub;
             s = bk ? -u[k] : s;
             cnt = bk ? T(0) : cnt;
