@@ -389,18 +389,21 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
 template <typename T, int E, int LPR, int WPL>
 __device__ __forceinline__ void seg_mean_c(T (&v)[E], uint32_t bnd, uint32_t pos, uint32_t neg,
                                            const Comm<T, LPR, WPL>& C, T& lam_part) {
-    // pass 1: lane-local segment sums at segment ends (the lane's first segment
-    // still lacks the carry) and the open tail
-    T s = T(0), sf = T(0);
-    bool hf = false;
+    // pass 1: means of the segments that end inside the lane; the lane's first
+    // segment keeps its partial sum (it still lacks the carry), the open tail sum
+    // goes to the scan
+    const uint32_t firstb = bnd & (0u - bnd);
+    T s = T(0), sf = T(0), cnt = T(0);
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         s += v[k];
+        cnt += T(1);
         const bool bk = bit<E>(bnd, k);
-        sf = (bk & !hf) ? s : sf;
-        hf = hf | bk;
-        v[k] = bk ? s : v[k];
+        const bool fk = bit<E>(firstb, k);
+        sf = fk ? s : sf;
+        v[k] = bk ? s * rcp_(cnt) : v[k];
         s = bk ? T(0) : s;
+        cnt = bk ? T(0) : cnt;
     }
     const int hb = 31 - __clz(bnd);
     const bool fl = bnd != 0u;
@@ -408,17 +411,8 @@ __device__ __forceinline__ void seg_mean_c(T (&v)[E], uint32_t bnd, uint32_t pos
     int cc = E - 1 - hb;
     C.template scan_fwd<0>(cs, cc, fl);
     const int fb = __ffs(bnd) - 1;
-    const uint32_t firstm = bnd ? ((bnd & (0u - bnd)) * 2u - 1u) : 0u;
+    const uint32_t firstm = bnd ? (firstb * 2u - 1u) : 0u;
     const T fv = (sf + cs) * rcp_(T(fb + 1 + cc));
-    // pass 2: means at segment ends
-    T cnt = T(0);
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-        cnt += T(1);
-        const bool bk = bit<E>(bnd, k);
-        v[k] = bk ? (bit<E>(firstm, k) ? fv : v[k] * rcp_(cnt)) : v[k];
-        cnt = bk ? T(0) : cnt;
-    }
     // pass 3 (reverse): broadcast each segment's mean to its samples
     T cur = C.template scan_rev<2>(fv, fl);
 #pragma unroll

@@ -16,7 +16,7 @@ for k in range(4):
     z, mask, it = tvprox.tv1d_fwd(A.reshape(P * H, W), lam_rows, want_iters=True, warm_mask=rm)
     itn = it.cpu().numpy()
     bad = np.where(itn < 0)[0]
-    print("k", k, "rows nonconv", len(bad), "stall", ((itn >> 16) & 1).sum(), "max", (itn & 0xffff).max())
+    print("k", k, "rows nonconv", len(bad), "stall", ((itn >> 16) & 1).sum(), "max", (itn & 0xffff).max(), "mean %.2f" % (itn & 0xffff).mean(), "hist", np.bincount(itn & 0xffff)[:8].tolist())
     for r in bad[:3]:
         saved.append(dict(kind='row', k=k, y=A.reshape(P*H, W)[r].cpu().numpy(), lam=float(lam_rows[r]), warm=None if rm is None else rm[r].cpu().numpy()))
     rm = mask
@@ -27,7 +27,7 @@ for k in range(4):
     yt, mask, it = tvprox.tv1d_fwd(Bt, lam_cols, want_iters=True, warm_mask=cm)
     itn = it.cpu().numpy()
     bad = np.where(itn < 0)[0]
-    print("k", k, "cols nonconv", len(bad), "stall", ((itn >> 16) & 1).sum(), "max", (itn & 0xffff).max())
+    print("k", k, "cols nonconv", len(bad), "stall", ((itn >> 16) & 1).sum(), "max", (itn & 0xffff).max(), "mean %.2f" % (itn & 0xffff).mean(), "hist", np.bincount(itn & 0xffff)[:8].tolist())
     for c in bad[:3]:
         saved.append(dict(kind='col', k=k, y=Bt[c].cpu().numpy(), lam=float(lam_cols[c]), warm=None if cm is None else cm[c].cpu().numpy()))
     cm = mask
