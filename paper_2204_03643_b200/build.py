@@ -42,10 +42,15 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, debug: bool = False) -> str:
-    """debug=True builds libtvprox_debug.so with -DTVP_DEBUG (per-iteration device printf)."""
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, debug: bool = False,
+          defines=(), out: str = None) -> str:
+    """debug=True builds libtvprox_debug.so with -DTVP_DEBUG (per-iteration device printf).
+    defines/out: a tuning variant (-D flags) built into its own directory and library (A/B only)."""
     bdir = BUILD + ("_debug" if debug else "")
     lib = LIB.replace(".so", "_debug.so") if debug else LIB
+    if out:
+        bdir = BUILD + "_" + os.path.splitext(os.path.basename(out))[0]
+        lib = os.path.abspath(out)
     os.makedirs(bdir, exist_ok=True)
     deps = _deps()
     if not force and not _stale(lib, deps):
@@ -57,7 +62,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, deb
         objs.append(obj)
         if force or _stale(obj, deps):
             cmd = [NVCC] + ARCH + FLAGS + (["-Xptxas", "-v"] if ptxas_v else []) + \
-                (["-DTVP_DEBUG"] if debug else []) + ["-c", src, "-o", obj]
+                (["-DTVP_DEBUG"] if debug else []) + ["-D" + d for d in defines] + ["-c", src, "-o", obj]
             jobs.append(cmd)
 
     def run(cmd):
@@ -88,5 +93,7 @@ if __name__ == "__main__":
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ptxas", action="store_true")
     ap.add_argument("--debug", action="store_true")
+    ap.add_argument("--define", action="append", default=[])
+    ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose, ptxas_v=a.ptxas, debug=a.debug))
+    print(build(force=a.force, verbose=a.verbose, ptxas_v=a.ptxas, debug=a.debug, defines=a.define, out=a.out))

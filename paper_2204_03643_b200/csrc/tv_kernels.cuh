@@ -35,6 +35,7 @@ struct RowFwdArgs {
     int mw;                    // mask words per line
     int32_t* row_iters;        // nullable
     int32_t* iters_max;        // nullable (2D diagnostics)
+    int coarse;                // cold solve: coarse initial bound set (coarse_init)
 };
 
 template <typename T>
@@ -54,6 +55,7 @@ struct ColFwdArgs {
     int mw;
     int TC;
     int32_t* iters_max;
+    int coarse;              // cold solve: coarse initial bound set (coarse_init)
 };
 
 template <typename T>
@@ -116,7 +118,8 @@ __device__ __forceinline__ void smem_to_regs(const T* buf, int l, T (&y)[E]) {
 template <typename T, int E, int LPR, int WPL, bool PE>
 __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& lam, int n,
                                           bool valid, uint32_t warm_pos, uint32_t warm_neg,
-                                          const Comm<T, LPR, WPL>& C) {
+                                          const Comm<T, LPR, WPL>& C, bool coarse = false,
+                                          T* xb = nullptr) {
     const int ll = C.w * LPR + C.l;           // line lane
     uint32_t pin = 0;
     bool bad = false;
@@ -141,6 +144,14 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
     T mean = active ? sum / T(n) : T(0);
 #pragma unroll
     for (int k = 0; k < E; ++k) y[k] -= mean;
+    // cold solve: initial bound set from the block-restricted problem (coarse_init);
+    // lines held by a full warp or more (short lines converge in 3-5 iterations cold)
+    if (!PE && LPR * WPL >= 32 && coarse && n / E >= 3) {
+        uint32_t cp, cn;
+        coarse_init<T, E, LPR, WPL>(y, lam.r, n, active, C, xb, cp, cn);
+        warm_pos |= cp;
+        warm_neg |= cn;
+    }
     T u[E];
     int st = pn_solve<T, E, LPR, WPL, PE>(y, u, w, pin, warm_pos, warm_neg, lam, C, active);
 #pragma unroll
@@ -152,11 +163,34 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
 // ===========================================================================
 // Row forward: 1D rows or Dykstra row pass.
 // ===========================================================================
-#ifndef TVP_ROW_MINB
-#define TVP_ROW_MINB 1
+// Minimum resident blocks per SM of the forward kernels (register caps measured by
+// same-box A/B: the issue-bound PN loops gain from occupancy until they would spill;
+// fp64 and the long-register-line geometries keep their natural allocation).
+// TVP_ROW_MINB / TVP_ROWW_MINB / TVP_COL_MINB override them for A/B builds.
+template <typename T, int E> constexpr int row_minb() {
+#ifdef TVP_ROW_MINB
+    return TVP_ROW_MINB;
+#else
+    return sizeof(T) == 4 ? (E <= 8 ? 6 : 1) : 1;
 #endif
+}
+template <typename T, int E, int WPL> constexpr int roww_minb() {
+#ifdef TVP_ROWW_MINB
+    return TVP_ROWW_MINB;
+#else
+    return (sizeof(T) == 4 && E == 16 && WPL == 2) ? 7 : 1;
+#endif
+}
+template <typename T, int E> constexpr int col_minb() {
+#ifdef TVP_COL_MINB
+    return TVP_COL_MINB;
+#else
+    return (sizeof(T) == 4 && E <= 8) ? 2 : 1;
+#endif
+}
+
 template <typename T, int E, int LPR, bool PE, bool DYK, int WPB>
-__global__ void __launch_bounds__(WPB * 32, TVP_ROW_MINB)
+__global__ void __launch_bounds__(WPB * 32, (row_minb<T, E>()))
 k_row_fwd(RowFwdArgs<T> a) {
     constexpr int G = 32 / LPR;
     constexpr int LP = line_pitch<E, LPR>();
@@ -219,7 +253,7 @@ k_row_fwd(RowFwdArgs<T> a) {
             mask_window<E>(a.mask_in + r * a.mw, a.mw, l * E, wb, wp, wn);
         }
         const Comm<T, LPR, 1> C{l, 0, nullptr, nullptr};
-        int st = solve_line<T, E, LPR, 1, PE>(y, w, lam, n, valid, wp, wn, C);
+        int st = solve_line<T, E, LPR, 1, PE>(y, w, lam, n, valid, wp, wn, C, a.coarse != 0);
         __syncwarp();
         if (valid) {
 #pragma unroll
@@ -270,11 +304,8 @@ k_row_fwd(RowFwdArgs<T> a) {
 // Row forward with WPL warps per line (E samples per lane, 32*WPL lanes per line):
 // the block is one line at a time; cross-warp scans through shared memory.
 // ===========================================================================
-#ifndef TVP_ROWW_MINB
-#define TVP_ROWW_MINB 6
-#endif
 template <typename T, int E, int WPL, bool PE, bool DYK>
-__global__ void __launch_bounds__(WPL * 32, TVP_ROWW_MINB)
+__global__ void __launch_bounds__(WPL * 32, (roww_minb<T, E, WPL>()))
 k_row_fwd_w(RowFwdArgs<T> a) {
     constexpr int NT = WPL * 32;
     constexpr int LP = line_pitch<E, NT>();
@@ -283,6 +314,7 @@ k_row_fwd_w(RowFwdArgs<T> a) {
     T* bufX = DYK ? bufA + LP : bufA;
     __shared__ T comm_v[kCommSlots * 3 * WPL];
     __shared__ int comm_i[kCommSlots * WPL];
+    __shared__ T coarse_v[32 * WPL];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Comm<T, 32, WPL> C{lane, warp, comm_v, comm_i};
     const int ll = threadIdx.x;                 // line lane
@@ -321,7 +353,7 @@ k_row_fwd_w(RowFwdArgs<T> a) {
             uint32_t wb;
             mask_window<E>(a.mask_in + r * a.mw, a.mw, ll * E, wb, wp, wn);
         }
-        int st = solve_line<T, E, 32, WPL, PE>(y, w, lam, n, true, wp, wn, C);
+        int st = solve_line<T, E, 32, WPL, PE>(y, w, lam, n, true, wp, wn, C, a.coarse != 0, coarse_v);
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < E; ++k) {
@@ -366,11 +398,8 @@ k_row_fwd_w(RowFwdArgs<T> a) {
 // ===========================================================================
 // Column forward: Dykstra column pass (tile of TC columns of one plane).
 // ===========================================================================
-#ifndef TVP_COL_MINB
-#define TVP_COL_MINB 1
-#endif
 template <typename T, int E, int LPR, int WPB>
-__global__ void __launch_bounds__(WPB * 32, TVP_COL_MINB)
+__global__ void __launch_bounds__(WPB * 32, (col_minb<T, E>()))
 k_col_fwd(ColFwdArgs<T> a) {
     constexpr int G = 32 / LPR;
     constexpr int LP = line_pitch<E, LPR>();
@@ -428,7 +457,7 @@ k_col_fwd(ColFwdArgs<T> a) {
                 mask_window<E>(a.mask_in + (p * W + c0 + c) * a.mw, a.mw, l * E, wb, wp, wn);
             }
             const Comm<T, LPR, 1> C{l, 0, nullptr, nullptr};
-            int st = solve_line<T, E, LPR, 1, false>(y, w, lam, H, valid, wp, wn, C);
+            int st = solve_line<T, E, LPR, 1, false>(y, w, lam, H, valid, wp, wn, C, a.coarse != 0);
             if (valid) {
 #pragma unroll
                 for (int k = 0; k < E; ++k) {

@@ -36,7 +36,7 @@ inline int lam_chunks(int64_t total, int64_t nout) {
     return (int)c;
 }
 
-template <typename T> cudaError_t launch_row_fwd(const RowFwdArgs<T>& a, bool per_edge, bool dykstra, cudaStream_t s);
+template <typename T> cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s);
 template <typename T> cudaError_t launch_col_fwd(ColFwdArgs<T> a, cudaStream_t s);
 template <typename T> cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s);
 template <typename T> cudaError_t launch_col_bwd(ColBwdArgs<T> a, cudaStream_t s);

@@ -72,7 +72,10 @@ static int row_fwd_split() {
     }
     return v;
 }
-constexpr int kColWPB = 8;
+#ifndef TVP_COL_WPB
+#define TVP_COL_WPB 8
+#endif
+constexpr int kColWPB = TVP_COL_WPB;
 
 template <typename T, int E, int LPR, bool PE, bool DYK>
 static cudaError_t row_fwd_t(const RowFwdArgs<T>& a, cudaStream_t s) {
@@ -98,9 +101,20 @@ static cudaError_t row_fwd_w_t(const RowFwdArgs<T>& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// TVP_COARSE=0 disables the coarse initial bound set of cold solves (A/B only).
+static bool coarse_knob() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TVP_COARSE");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v != 0;
+}
+
 template <typename T>
-cudaError_t launch_row_fwd(const RowFwdArgs<T>& a, bool per_edge, bool dykstra, cudaStream_t s) {
+cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
+    a.coarse = (a.mask_in == nullptr && !per_edge && coarse_knob()) ? 1 : 0;
     const int split = row_fwd_split();
     if (a.n > 512 && split == 2) {               // 1024-sample lines: two warps x 16 samples per lane
         if (dykstra) return row_fwd_w_t<T, 16, 2, false, true>(a, s);
@@ -144,6 +158,7 @@ static cudaError_t col_fwd_t(ColFwdArgs<T> a, cudaStream_t s) {
 template <typename T>
 cudaError_t launch_col_fwd(ColFwdArgs<T> a, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
+    a.coarse = (a.mask_in == nullptr && coarse_knob()) ? 1 : 0;
     TVP_GEO_DISPATCH(a.H, { e = col_fwd_t<T, E_, L_>(a, s); });
     return e;
 }
@@ -245,7 +260,7 @@ cudaError_t launch_axpby(const T* x, T* y, T a, T b, int64_t n, cudaStream_t s) 
 }
 
 #define TVP_INSTANTIATE(T)                                                                         \
-    template cudaError_t launch_row_fwd<T>(const RowFwdArgs<T>&, bool, bool, cudaStream_t);        \
+    template cudaError_t launch_row_fwd<T>(RowFwdArgs<T>, bool, bool, cudaStream_t);        \
     template cudaError_t launch_col_fwd<T>(ColFwdArgs<T>, cudaStream_t);                           \
     template cudaError_t launch_row_bwd<T>(const RowBwdArgs<T>&, bool, bool, cudaStream_t);        \
     template cudaError_t launch_col_bwd<T>(ColBwdArgs<T>, cudaStream_t);                           \

@@ -379,6 +379,73 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
 }
 
 // ---------------------------------------------------------------------------
+// Coarse initial bound set for a cold solve (reading O7).  The line is
+// cut into the lanes' blocks of E samples; restricting x to be constant on full
+// blocks turns Eq. 1 into the same prox on the block means with lam / E:
+//     1/2 sum_b E (x_b - ybar_b)^2 + lam sum_b |x_{b+1} - x_b|.
+// That nc = n / E sample problem is solved by the same projected Newton method
+// (pn_solve), and its jumps become the initial bound edges of the fine solve
+// (u = +lam on an up jump, -lam on a down jump, at the block's last edge).  Only
+// the PN iteration count depends on this; the fine solve's answer does not.
+//   WPL == 1: coarse sample b is held by line lane b (one per lane, in place).
+//   WPL  > 1: block means are exchanged through xb[32*WPL] (shared memory) and
+//             every warp solves the whole coarse line redundantly (WPL samples
+//             per lane, warp shuffles only); jump bits come back by ballots.
+// ---------------------------------------------------------------------------
+template <typename T, int E, int LPR, int WPL>
+__device__ __forceinline__ void coarse_init(const T (&y)[E], T lam_r, int n, bool active,
+                                            const Comm<T, LPR, WPL>& C, T* xb,
+                                            uint32_t& cpos, uint32_t& cneg) {
+    const int ll = C.w * LPR + C.l;
+    const int nc = n / E;
+    T bs = T(0);
+#pragma unroll
+    for (int k = 0; k < E; ++k) bs += y[k];
+    const T ybar = (ll < nc) ? bs * (T(1) / T(E)) : T(0);
+    Lam<T, WPL, false> lc;
+    lc.r = lam_r * (T(1) / T(E));
+    constexpr uint32_t top = 1u << (E - 1);
+    cpos = cneg = 0u;
+    if constexpr (WPL == 1) {
+        T yc[WPL], uc[WPL], wc[WPL];
+        yc[0] = ybar;
+        const uint32_t pinc = (ll >= nc - 1) ? 1u : 0u;
+        pn_solve<T, WPL, LPR, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active);
+        const T xn = shdn<LPR>(wc[0], 1);
+        if (ll < nc - 1) {
+            cpos = xn > wc[0] ? top : 0u;
+            cneg = xn < wc[0] ? top : 0u;
+        }
+    } else {
+        xb[ll] = ybar;
+        __syncthreads();
+        const int l = C.l;
+        T yc[WPL], uc[WPL], wc[WPL];
+        uint32_t pinc = 0u;
+#pragma unroll
+        for (int q = 0; q < WPL; ++q) {
+            yc[q] = xb[l * WPL + q];
+            pinc |= (l * WPL + q >= nc - 1) ? (1u << q) : 0u;
+        }
+        const Comm<T, 32, 1> Cw{l, 0, nullptr, nullptr};
+        pn_solve<T, WPL, 32, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, Cw, active);
+        const T xn = shdn<32>(wc[0], 1);
+        const int cl = ll / WPL, cq = ll % WPL;
+#pragma unroll
+        for (int q = 0; q < WPL; ++q) {
+            const T nx = (q + 1 < WPL) ? wc[(q + 1 < WPL) ? q + 1 : q] : xn;
+            const bool inl = l * WPL + q < nc - 1;
+            const uint32_t bu = __ballot_sync(FULL, inl && nx > wc[q]);
+            const uint32_t bd = __ballot_sync(FULL, inl && nx < wc[q]);
+            if (q == cq) {
+                cpos = ((bu >> cl) & 1u) ? top : 0u;
+                cneg = ((bd >> cl) & 1u) ? top : 0u;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Backward primitive: v <- segment-wise mean of v (Eq. 7 under reading O12:
 // the symmetric projector onto vectors constant on the segments), for a line
 // held by a Comm group.  Segments end at edges in `bnd`; the jump sign of edge

@@ -1,0 +1,132 @@
+"""Vectorised fp64 model of the kernel's fast-mode PN (projected full Newton steps from
+the partition candidate) to count iterations under different initial bound sets.
+Research aid only (not product, not a test)."""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, '.')
+import oracle  # noqa: E402
+from paper_2204_03643_b200 import workloads  # noqa: E402
+
+
+def candidate(y, u, bnd):
+    """Partition candidate of a bound set (bnd[n-1] must be True): xhat, uhat."""
+    n = len(y)
+    ends = np.flatnonzero(bnd)
+    starts = np.concatenate([[0], ends[:-1] + 1])
+    ssum = np.add.reduceat(y, starts)
+    uR = u[ends]
+    uL = np.concatenate([[0.0], uR[:-1]])
+    ln = ends - starts + 1
+    val = (ssum + uR - uL) / ln
+    xh = np.repeat(val, ln)
+    # uhat_i = uL + sum_{a..i}(xh - y)
+    seg = np.repeat(np.arange(len(ln)), ln)
+    c = np.cumsum(xh - y)
+    cstart = np.concatenate([[0.0], c[ends[:-1]]])
+    uh = uL[seg] + c - cstart[seg]
+    return xh, uh
+
+
+def pn(y, lam, init_pos=None, init_neg=None, maxit=64):
+    n = len(y)
+    y = y - y.mean()
+    pin = np.zeros(n, bool)
+    pin[n - 1] = True
+    u = np.zeros(n)
+    bnd = pin.copy()
+    if init_pos is not None:
+        u[init_pos] = lam
+        u[init_neg] = -lam
+        bnd |= init_pos | init_neg
+    first = True
+    for it in range(maxit):
+        if not first:
+            x = y + u - np.concatenate([[0], u[:-1]])
+            g = np.append(np.diff(x), 0)
+            bnd = pin | ((np.abs(u) >= lam) & (u * g > 0))
+        xh, uh = candidate(y, u, bnd)
+        free = ~bnd
+        feas = np.all(np.abs(uh[free]) <= lam * (1 + 1e-12) + 1e-12)
+        jb = bnd & ~pin
+        dx = np.append(np.diff(xh), 0)
+        sgn = np.all(u[jb] * dx[jb] >= -1e-12)
+        if feas and sgn:
+            return xh, it + 1
+        u = np.where(bnd, u, np.clip(uh, -lam, lam))
+        first = False
+    return xh, maxit
+
+
+def coarse_init(y, lam, m):
+    """Bound set from the exact prox of the m-block means with lam/m (block-constant restriction)."""
+    n = len(y)
+    nb = n // m
+    yb = y[:nb * m].reshape(nb, m).mean(1)
+    xb = oracle.prox1d(yb, lam / m)
+    d = np.diff(xb)
+    pos = np.zeros(n, bool)
+    neg = np.zeros(n, bool)
+    e = np.arange(nb - 1) * m + m - 1
+    pos[e[d > 0]] = True
+    neg[e[d < 0]] = True
+    return pos, neg
+
+
+if __name__ == "__main__":
+    w = workloads.c2(batch=256)
+    res = {}
+    for name in ("cold", "coarse16", "coarse8", "coarse32"):
+        its = []
+        errs = []
+        for b in range(256):
+            y = w.y[b].astype(np.float64)
+            lam = float(w.lam[b])
+            if name == "cold":
+                xh, it = pn(y, lam)
+            else:
+                m = int(name[6:])
+                p, q = coarse_init(y, lam, m)
+                xh, it = pn(y, lam, p, q)
+            ref = oracle.prox1d(y, lam)
+            errs.append(np.abs(xh + y.mean() - ref).max())
+            its.append(it)
+        its = np.array(its)
+        print("%-9s iters mean %.2f (even %.2f odd %.2f) p99 %d max %d  maxerr %.1e" % (
+            name, its.mean(), its[::2].mean(), its[1::2].mean(), np.percentile(its, 99), its.max(), max(errs)))
+
+
+def coarse_pn_init(y, lam, m, inner=None):
+    """Coarse bound set from PN on the m-block means (lam/m); returns (pos, neg, coarse iters)."""
+    n = len(y)
+    nb = n // m
+    yb = y[:nb * m].reshape(nb, m).mean(1)
+    if inner:
+        p2, q2, it2 = coarse_pn_init(yb, lam / m, inner)
+        xb, itc = pn(yb, lam / m, p2, q2)
+    else:
+        xb, itc = pn(yb, lam / m)
+        it2 = 0
+    d = np.diff(xb)
+    pos = np.zeros(n, bool)
+    neg = np.zeros(n, bool)
+    e = np.arange(nb - 1) * m + m - 1
+    pos[e[d > 1e-12]] = True
+    neg[e[d < -1e-12]] = True
+    return pos, neg, (itc, it2)
+
+
+def run2():
+    w = workloads.c2(batch=256)
+    for m, inner in ((16, None), (8, None), (4, None), (8, 4), (16, 4), (32, None)):
+        its, cits, c2its = [], [], []
+        for b in range(256):
+            y = w.y[b].astype(np.float64)
+            lam = float(w.lam[b])
+            p, q, (itc, it2) = coarse_pn_init(y, lam, m, inner)
+            xh, it = pn(y, lam, p, q)
+            its.append(it); cits.append(itc); c2its.append(it2)
+        its = np.array(its)
+        print("m=%d inner=%s fine mean %.2f p99 %d max %d | coarse mean %.2f max %d | inner mean %.2f" % (
+            m, inner, its.mean(), np.percentile(its, 99), its.max(), np.mean(cits), max(cits), np.mean(c2its)))
