@@ -102,20 +102,28 @@ __device__ __forceinline__ uint32_t compact_even(uint32_t x) {
 // Extract the 2E-bit window of mask codes for edges [e0, e0+E) of one line
 // (word array `mw`, nw words).  Returns per-edge bitmasks: bnd = code != 0,
 // neg = code == DOWN, pos = code == UP (bit-parallel: lo/hi code bits, then
-// even-bit compaction, 16 edges per step).
+// even-bit compaction, 16 edges per step).  Split into the word loads
+// (mask_words_ld, issued early to overlap their latency) and the decode.
+template <int E> struct MaskWin {
+    static constexpr int NS = (2 * E + 31) / 32;   // words of the aligned window
+    uint32_t w[NS + 1];
+};
+
 template <int E>
-__device__ __forceinline__ void mask_window(const uint32_t* __restrict__ mw, int nw, int e0,
-                                            uint32_t& bnd, uint32_t& pos, uint32_t& neg) {
+__device__ __forceinline__ void mask_words_ld(const uint32_t* __restrict__ mw, int nw, int e0, MaskWin<E>& mwin) {
     const int w0 = e0 >> 4;
-    const int sh = (e0 & 15) * 2;
-    constexpr int NS = (2 * E + 31) / 32;   // words of the aligned window
-    uint32_t words[NS + 1];
 #pragma unroll
-    for (int j = 0; j <= NS; ++j) words[j] = (w0 + j < nw) ? __ldg(mw + w0 + j) : 0u;
+    for (int j = 0; j <= MaskWin<E>::NS; ++j) mwin.w[j] = (w0 + j < nw) ? __ldg(mw + w0 + j) : 0u;
+}
+
+template <int E>
+__device__ __forceinline__ void mask_decode(const MaskWin<E>& mwin, int e0, uint32_t& bnd, uint32_t& pos,
+                                            uint32_t& neg) {
+    const int sh = (e0 & 15) * 2;
     bnd = pos = neg = 0;
 #pragma unroll
-    for (int j = 0; j < NS; ++j) {
-        const uint32_t c = __funnelshift_r(words[j], words[j + 1], sh);   // 16 codes
+    for (int j = 0; j < MaskWin<E>::NS; ++j) {
+        const uint32_t c = __funnelshift_r(mwin.w[j], mwin.w[j + 1], sh);   // 16 codes
         const uint32_t lo = compact_even(c), hi = compact_even(c >> 1);
         bnd |= (lo | hi) << (16 * j);
         pos |= (lo & ~hi) << (16 * j);
@@ -123,6 +131,14 @@ __device__ __forceinline__ void mask_window(const uint32_t* __restrict__ mw, int
     }
     constexpr uint32_t m = (E >= 32) ? 0xffffffffu : ((1u << (E & 31)) - 1u);
     bnd &= m; pos &= m; neg &= m;
+}
+
+template <int E>
+__device__ __forceinline__ void mask_window(const uint32_t* __restrict__ mw, int nw, int e0,
+                                            uint32_t& bnd, uint32_t& pos, uint32_t& neg) {
+    MaskWin<E> mwin;
+    mask_words_ld<E>(mw, nw, e0, mwin);
+    mask_decode<E>(mwin, e0, bnd, pos, neg);
 }
 
 }  // namespace tvp

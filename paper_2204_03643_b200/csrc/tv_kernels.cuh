@@ -653,35 +653,49 @@ k_row_bwd_w(RowBwdArgs<T> a) {
     const bool vec = ((a.stride & 3) == 0) &&
                      ((reinterpret_cast<uintptr_t>(a.out) | reinterpret_cast<uintptr_t>(DYK ? a.B : a.A) |
                        reinterpret_cast<uintptr_t>(DYK && a.A ? a.A : a.out)) & 15) == 0;
-    for (int64_t r = blockIdx.x; r < a.nlines; r += gridDim.x) {
-        T v[E], pb[E];
+    // software pipeline: the next line's inputs and mask words are loaded into
+    // registers before the current line is reduced, so every block keeps one line
+    // of loads in flight while it computes (HBM latency hiding, Little's law).
+    T vn[E], pn[E];
+    MaskWin<E> mn;
+    auto load = [&](int64_t r) {
         if (DYK) {
-            ld_contig<T, E>(a.B + r * a.stride, i0, n, vec, v);
-            if (a.A) {
-                ld_contig<T, E>(a.A + r * a.stride, i0, n, vec, pb);
-#pragma unroll
-                for (int k = 0; k < E; ++k) v[k] -= pb[k];
-            } else {
-#pragma unroll
-                for (int k = 0; k < E; ++k) pb[k] = T(0);
-            }
+            ld_contig<T, E>(a.B + r * a.stride, i0, n, vec, vn);
+            if (a.A) ld_contig<T, E>(a.A + r * a.stride, i0, n, vec, pn);
         } else {
-            ld_contig<T, E>(a.A + r * a.stride, i0, n, vec, v);
+            ld_contig<T, E>(a.A + r * a.stride, i0, n, vec, vn);
+        }
+        if (a.mw > 0) mask_words_ld<E>(a.mask + r * a.mw, a.mw, i0, mn);
+    };
+    int64_t r = blockIdx.x;
+    if (r < a.nlines) load(r);
+    for (; r < a.nlines; r += gridDim.x) {
+        T v[E], pb[E];
+        MaskWin<E> mc = mn;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            v[k] = vn[k];
+            pb[k] = (DYK && a.A) ? pn[k] : T(0);
+        }
+        if (r + gridDim.x < a.nlines) load(r + gridDim.x);
+        if (DYK) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) v[k] -= pb[k];
         }
         uint32_t bnd = 0, pos = 0, neg = 0;
-        if (a.mw > 0) mask_window<E>(a.mask + r * a.mw, a.mw, i0, bnd, pos, neg);
+        if (a.mw > 0) mask_decode<E>(mc, i0, bnd, pos, neg);
 #pragma unroll
         for (int k = 0; k < E; ++k)
             if (i0 + k >= n - 1) bnd |= 1u << k;
         T lp = T(0);
         seg_mean_c<T, E, 32, WPL>(v, bnd, pos, neg, C, lp);
         if (PE) {
-            const T vn = C.template next<4>(v[0]);
+            const T vnx = C.template next<4>(v[0]);
             if (a.lam_edge) {
 #pragma unroll
                 for (int k = 0; k < E; ++k) {
                     const int e = i0 + k;
-                    const T nxt = (k + 1 < E) ? v[(k + 1 < E) ? k + 1 : k] : vn;
+                    const T nxt = (k + 1 < E) ? v[(k + 1 < E) ? k + 1 : k] : vnx;
                     if (e < n - 1) {
                         const T sg = bit<E>(pos, k) ? T(1) : (bit<E>(neg, k) ? T(-1) : T(0));
                         a.lam_edge[r * a.stride + e] = sg * (v[k] - nxt);

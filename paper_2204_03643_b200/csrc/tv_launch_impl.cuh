@@ -188,6 +188,18 @@ static cudaError_t row_bwd_w_t(const RowBwdArgs<T>& a, cudaStream_t s) {
 template <typename T>
 cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
+    // TVP_BWD_SPLIT (A/B): warps per long line; default 2 x 16 samples (measured best for n = 1024)
+    static const int bsplit = getenv("TVP_BWD_SPLIT") ? atoi(getenv("TVP_BWD_SPLIT")) : 2;
+    if (a.n > 512 && bsplit == 1) {               // A/B: 1 warp x 32 samples per thread
+        if (dykstra) return row_bwd_w_t<T, 32, 1, true, false>(a, s);
+        if (per_edge) return row_bwd_w_t<T, 32, 1, false, true>(a, s);
+        return row_bwd_w_t<T, 32, 1, false, false>(a, s);
+    }
+    if (a.n > 512 && bsplit == 2) {               // A/B: 2 warps x 16 samples per thread
+        if (dykstra) return row_bwd_w_t<T, 16, 2, true, false>(a, s);
+        if (per_edge) return row_bwd_w_t<T, 16, 2, false, true>(a, s);
+        return row_bwd_w_t<T, 16, 2, false, false>(a, s);
+    }
     if (a.n > 512) {                              // long lines: 4 warps x 8 samples per thread
         if (dykstra) return row_bwd_w_t<T, 8, 4, true, false>(a, s);
         if (per_edge) return row_bwd_w_t<T, 8, 4, false, true>(a, s);
