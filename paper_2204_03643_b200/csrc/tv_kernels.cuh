@@ -99,6 +99,35 @@ __device__ __forceinline__ T line_lambda(const T* lam, int mode, T scalar, int64
     }
 }
 
+// Contiguous per-lane loads / stores of E samples starting at i0 (16-byte vectors
+// when aligned and in range; scalar with bounds otherwise).
+template <typename T, int E>
+__device__ __forceinline__ void ld_contig(const T* __restrict__ p, int i0, int n, bool vec, T (&v)[E]) {
+    if (sizeof(T) == 4 && (E % 4) == 0 && vec && i0 + E <= n) {
+#pragma unroll
+        for (int q = 0; q < E / 4; ++q) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(p + i0) + q);
+            v[4 * q + 0] = (T)f.x; v[4 * q + 1] = (T)f.y; v[4 * q + 2] = (T)f.z; v[4 * q + 3] = (T)f.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = (i0 + k < n) ? __ldg(p + i0 + k) : T(0);
+    }
+}
+template <typename T, int E>
+__device__ __forceinline__ void st_contig(T* __restrict__ p, int i0, int n, bool vec, const T (&v)[E]) {
+    if (sizeof(T) == 4 && (E % 4) == 0 && vec && i0 + E <= n) {
+#pragma unroll
+        for (int q = 0; q < E / 4; ++q)
+            reinterpret_cast<float4*>(p + i0)[q] = make_float4((float)v[4 * q], (float)v[4 * q + 1],
+                                                              (float)v[4 * q + 2], (float)v[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+            if (i0 + k < n) p[i0 + k] = v[k];
+    }
+}
+
 // Odd pitch of one staged line in shared memory (conflict-free lane reads).
 template <int E, int LPR>
 __host__ __device__ constexpr int line_pitch() {
@@ -307,43 +336,47 @@ k_row_fwd(RowFwdArgs<T> a) {
 template <typename T, int E, int WPL, bool PE, bool DYK>
 __global__ void __launch_bounds__(WPL * 32, (roww_minb<T, E, WPL>()))
 k_row_fwd_w(RowFwdArgs<T> a) {
+    // Each line lane holds E contiguous samples loaded straight from HBM into
+    // registers (16-byte vectors when aligned) and stores its outputs the same way;
+    // no shared-memory staging, so the block's code stays small (the PN loop is
+    // instruction-cache bound).  E == 16: a lane's 16 edges
+    // are exactly one 32-bit mask word, written by that lane.
+    static_assert(E % 16 == 0 || 16 % E == 0, "mask words per lane");
     constexpr int NT = WPL * 32;
-    constexpr int LP = line_pitch<E, NT>();
-    extern __shared__ __align__(16) unsigned char smraw_[];
-    T* bufA = reinterpret_cast<T*>(smraw_);
-    T* bufX = DYK ? bufA + LP : bufA;
     __shared__ T comm_v[kCommSlots * 3 * WPL];
     __shared__ int comm_i[kCommSlots * WPL];
     __shared__ T coarse_v[32 * WPL];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Comm<T, 32, WPL> C{lane, warp, comm_v, comm_i};
     const int ll = threadIdx.x;                 // line lane
+    const int i0 = ll * E;
     const int n = a.n;
+    (void)NT;
+    const bool vec = ((a.stride & 3) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(a.src0) | reinterpret_cast<uintptr_t>(a.dst0) |
+                       reinterpret_cast<uintptr_t>(DYK && a.src1 ? a.src1 : a.src0) |
+                       reinterpret_cast<uintptr_t>(DYK && a.dst1 ? a.dst1 : a.dst0) |
+                       reinterpret_cast<uintptr_t>(PE ? a.lam : a.src0)) & 15) == 0;
     for (int64_t r = blockIdx.x; r < a.nlines; r += gridDim.x) {
-        const T* s0 = a.src0 + r * a.stride;
-        const T* s1 = (DYK && a.src1) ? a.src1 + r * a.stride : nullptr;
-        {
-            T v0[E], v1[E];
+        T y[E], w[E];
+        ld_contig<T, E>(a.src0 + r * a.stride, i0, n, vec, y);
+        T akeep[DYK ? E : 1];
+        if (DYK) {
+            if (a.src1) {
+                T p[E];
+                ld_contig<T, E>(a.src1 + r * a.stride, i0, n, vec, p);
 #pragma unroll
-            for (int q = 0; q < E; ++q) {
-                const int i = q * NT + ll;
-                const bool in = i < n;
-                v0[q] = in ? __ldg(s0 + i) : T(0);
-                v1[q] = (DYK && s1 && in) ? __ldg(s1 + i) : T(0);
+                for (int k = 0; k < E; ++k) y[k] += p[k];
             }
 #pragma unroll
-            for (int q = 0; q < E; ++q) bufA[spad(q * NT + ll)] = DYK ? v0[q] + v1[q] : v0[q];
+            for (int k = 0; k < E; ++k) akeep[DYK ? k : 0] = y[k];
         }
-        __syncthreads();
-        T y[E], w[E];
-        smem_to_regs<T, E>(bufA, ll, y);
         Lam<T, E, PE> lam;
         if (PE) {
+            T le[E];
+            ld_contig<T, E>(a.lam + r * a.stride, i0, n - 1, vec, le);
 #pragma unroll
-            for (int k = 0; k < E; ++k) {
-                int e = ll * E + k;
-                lam.e[PE ? k : 0] = (e < n - 1) ? __ldg(a.lam + r * a.stride + e) : T(0);
-            }
+            for (int k = 0; k < E; ++k) lam.e[PE ? k : 0] = le[k];
             lam.r = T(0);
         } else {
             lam.r = line_lambda(a.lam, a.lam_mode, a.lam_scalar, r, a.lines_per_plane, a.C);
@@ -351,47 +384,54 @@ k_row_fwd_w(RowFwdArgs<T> a) {
         uint32_t wp = 0, wn = 0;
         if (a.mask_in && a.mw > 0) {
             uint32_t wb;
-            mask_window<E>(a.mask_in + r * a.mw, a.mw, ll * E, wb, wp, wn);
+            mask_window<E>(a.mask_in + r * a.mw, a.mw, i0, wb, wp, wn);
         }
-        int st = solve_line<T, E, 32, WPL, PE>(y, w, lam, n, true, wp, wn, C, a.coarse != 0, coarse_v);
-        __syncthreads();
+        const int st = solve_line<T, E, 32, WPL, PE>(y, w, lam, n, true, wp, wn, C, a.coarse != 0, coarse_v);
+        st_contig<T, E>(a.dst0 + r * a.stride, i0, n, vec, w);
+        if (DYK && a.dst1) {
+            T p[E];
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-            int i = ll * E + k;
-            if (i < n) bufX[spad(i)] = w[k];
-        }
-        __syncthreads();
-        T* d0 = a.dst0 + r * a.stride;
-        T* d1 = DYK && a.dst1 ? a.dst1 + r * a.stride : nullptr;
-#pragma unroll
-        for (int q = 0; q < E; ++q) {
-            const int i = q * NT + ll;
-            if (i < n) {
-                T xv = bufX[spad(i)];
-                d0[i] = xv;
-                if (DYK && d1) d1[i] = bufA[spad(i)] - xv;
-            }
+            for (int k = 0; k < E; ++k) p[k] = akeep[DYK ? k : 0] - w[k];
+            st_contig<T, E>(a.dst1 + r * a.stride, i0, n, vec, p);
         }
         if (a.mask_out) {
-            T lz_line = PE ? T(1) : line_lambda(a.lam, a.lam_mode, a.lam_scalar, r, a.lines_per_plane, a.C);
-            for (int wd = ll; wd < a.mw; wd += NT) {
-                uint32_t word = 0;
-#pragma unroll 4
-                for (int q = 0; q < 16; ++q) {
-                    int e = wd * 16 + q;
-                    if (e < n - 1) {
-                        T le = PE ? __ldg(a.lam + r * a.stride + e) : lz_line;
-                        word |= edge_code(bufX[spad(e)], bufX[spad(e + 1)], !(le > T(0))) << (2 * q);
+            // 2-bit codes of the lane's edges i0 .. i0+E-1 (edge e between samples e, e+1)
+            const T wnext = C.template next<11>(w[0]);
+            uint32_t word = 0;
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnext;
+                const bool lz = PE ? !(lam.e[PE ? k : 0] > T(0)) : !(lam.r > T(0));
+                const uint32_t code = (i0 + k < n - 1) ? edge_code(w[k], xr, lz) : 0u;
+                word |= code << (2 * ((i0 + k) & 15));
+            }
+            if (E < 16) {               // 16 / E lanes share one word
+#pragma unroll
+                for (int d = 1; d < 16 / (E < 16 ? E : 16); d <<= 1) word |= __shfl_xor_sync(FULL, word, d);
+            }
+            const int wd = i0 >> 4;
+            if (wd < a.mw && (E >= 16 || (i0 & 15) == 0)) {
+#pragma unroll
+                for (int j = 0; j < (E + 15) / 16; ++j) {
+                    uint32_t wj = word;
+                    if (E > 16) {       // (E a multiple of 16) -- recompute the j-th word
+                        wj = 0;
+#pragma unroll
+                        for (int k = 16 * j; k < 16 * j + 16 && k < E; ++k) {
+                            const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnext;
+                            const bool lz = PE ? !(lam.e[PE ? k : 0] > T(0)) : !(lam.r > T(0));
+                            const uint32_t code = (i0 + k < n - 1) ? edge_code(w[k], xr, lz) : 0u;
+                            wj |= code << (2 * (k - 16 * j));
+                        }
                     }
+                    if (wd + j < a.mw) a.mask_out[r * a.mw + wd + j] = wj;
                 }
-                a.mask_out[r * a.mw + wd] = word;
             }
         }
         if (ll == 0) {
             if (a.row_iters) a.row_iters[r] = st;
             if (a.iters_max) atomicMax(a.iters_max, st >= 0 ? (st & 0xffff) : (1 << 20));
         }
-        __syncthreads();
     }
 }
 
@@ -613,33 +653,6 @@ k_row_bwd(RowBwdArgs<T> a) {
 // vector loads when aligned), segment mean through the Comm group, 16-byte
 // stores.  No shared-memory staging.
 // ===========================================================================
-template <typename T, int E>
-__device__ __forceinline__ void ld_contig(const T* __restrict__ p, int i0, int n, bool vec, T (&v)[E]) {
-    if (sizeof(T) == 4 && (E % 4) == 0 && vec && i0 + E <= n) {
-#pragma unroll
-        for (int q = 0; q < E / 4; ++q) {
-            const float4 f = __ldg(reinterpret_cast<const float4*>(p + i0) + q);
-            v[4 * q + 0] = (T)f.x; v[4 * q + 1] = (T)f.y; v[4 * q + 2] = (T)f.z; v[4 * q + 3] = (T)f.w;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < E; ++k) v[k] = (i0 + k < n) ? __ldg(p + i0 + k) : T(0);
-    }
-}
-template <typename T, int E>
-__device__ __forceinline__ void st_contig(T* __restrict__ p, int i0, int n, bool vec, const T (&v)[E]) {
-    if (sizeof(T) == 4 && (E % 4) == 0 && vec && i0 + E <= n) {
-#pragma unroll
-        for (int q = 0; q < E / 4; ++q)
-            reinterpret_cast<float4*>(p + i0)[q] = make_float4((float)v[4 * q], (float)v[4 * q + 1],
-                                                              (float)v[4 * q + 2], (float)v[4 * q + 3]);
-    } else {
-#pragma unroll
-        for (int k = 0; k < E; ++k)
-            if (i0 + k < n) p[i0 + k] = v[k];
-    }
-}
-
 template <typename T, int E, int WPL, bool DYK, bool PE>
 __global__ void __launch_bounds__(WPL * 32)
 k_row_bwd_w(RowBwdArgs<T> a) {

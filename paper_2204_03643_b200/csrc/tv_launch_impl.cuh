@@ -92,11 +92,9 @@ static cudaError_t row_fwd_t(const RowFwdArgs<T>& a, cudaStream_t s) {
 
 template <typename T, int E, int WPL, bool PE, bool DYK>
 static cudaError_t row_fwd_w_t(const RowFwdArgs<T>& a, cudaStream_t s) {
-    constexpr int LP = line_pitch<E, 32 * WPL>();
-    const size_t smem = (size_t)(DYK ? 2 : 1) * LP * sizeof(T);
     auto kern = k_row_fwd_w<T, E, WPL, PE, DYK>;
-    const int grid = persistent_grid(kern, WPL * 32, smem, a.nlines);
-    kern<<<grid, WPL * 32, smem, s>>>(a);
+    const int grid = persistent_grid(kern, WPL * 32, 0, a.nlines);
+    kern<<<grid, WPL * 32, 0, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }
