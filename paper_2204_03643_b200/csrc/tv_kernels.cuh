@@ -436,6 +436,65 @@ k_row_fwd_w(RowFwdArgs<T> a) {
 }
 
 // ===========================================================================
+// Coarse pre-pass of the long-row forward (reading O7): one
+// warp per line solves the block-restricted problem (block means of EF = 16
+// samples, lam / 16) by projected Newton and writes its jumps as an initial mask
+// (code at each block's last edge, 0 elsewhere) into the caller's mask buffer; the
+// fine kernel then starts from it as a warm start and overwrites the mask.  Kept
+// out of the fine kernel so that the hot PN loop owns the instruction cache.
+// ===========================================================================
+template <typename T, int CPL, bool DYK, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_coarse_rows(RowFwdArgs<T> a) {
+    constexpr int EF = 16;                  // fine samples per coarse block (= fine E)
+    constexpr int E = EF * CPL;             // samples per lane here
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = a.n, i0 = lane * E;
+    const int nc = n / EF;
+    const bool vec = ((a.stride & 3) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(a.src0) |
+                       reinterpret_cast<uintptr_t>(DYK && a.src1 ? a.src1 : a.src0)) & 15) == 0;
+    const Comm<T, 32, 1> C{lane, 0, nullptr, nullptr};
+    for (int64_t r = (int64_t)blockIdx.x * WPB + warp; r < a.nlines; r += (int64_t)gridDim.x * WPB) {
+        T v[E];
+        ld_contig<T, E>(a.src0 + r * a.stride, i0, n, vec, v);
+        if (DYK && a.src1) {
+            T p[E];
+            ld_contig<T, E>(a.src1 + r * a.stride, i0, n, vec, p);
+#pragma unroll
+            for (int k = 0; k < E; ++k) v[k] += p[k];
+        }
+        T yc[CPL], uc[CPL], wc[CPL];
+        uint32_t pinc = 0u;
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+            T sm = T(0);
+#pragma unroll
+            for (int k = 0; k < EF; ++k) {
+                sm += v[q * EF + k];
+                bad = bad || !finite_(v[q * EF + k]);
+            }
+            const int j = lane * CPL + q;
+            yc[q] = (j < nc) ? sm * (T(1) / T(EF)) : T(0);
+            pinc |= (j >= nc - 1) ? (1u << q) : 0u;
+        }
+        const T lam = line_lambda(a.lam, a.lam_mode, a.lam_scalar, r, a.lines_per_plane, a.C);
+        const bool active = !__any_sync(FULL, bad) && lam > T(0) && nc >= 3;
+        Lam<T, CPL, false> lc;
+        lc.r = lam * (T(1) / T(EF));
+        pn_solve<T, CPL, 32, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active);
+        const T xn = shdn<32>(wc[0], 1);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+            const int j = lane * CPL + q;            // coarse edge j = fine edge 16 j + 15 = word j, bits 30..31
+            const T nx = (q + 1 < CPL) ? wc[(q + 1 < CPL) ? q + 1 : q] : xn;
+            const uint32_t code = (active && j < nc - 1) ? (nx > wc[q] ? CODE_UP : (nx < wc[q] ? CODE_DOWN : 0u)) : 0u;
+            if (j < a.mw) a.mask_out[r * a.mw + j] = code << 30;
+        }
+    }
+}
+
+// ===========================================================================
 // Column forward: Dykstra column pass (tile of TC columns of one plane).
 // ===========================================================================
 template <typename T, int E, int LPR, int WPB>

@@ -109,11 +109,39 @@ static bool coarse_knob() {
     return v != 0;
 }
 
+// Coarse pre-pass for the long-row geometry (E = 16 fine blocks): writes the initial
+// mask into mask_out, which the fine kernel then reads as its warm start.
+template <typename T, bool DYK>
+static cudaError_t coarse_rows_t(const RowFwdArgs<T>& a, cudaStream_t s) {
+    constexpr int WPB = 4;
+    auto kern = k_coarse_rows<T, 2, DYK, WPB>;
+    const int grid = persistent_grid(kern, WPB * 32, 0, (a.nlines + WPB - 1) / WPB);
+    kern<<<grid, WPB * 32, 0, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// TVP_COARSE_PASS=0 keeps the coarse solve inside the long-row forward kernel (A/B).
+static bool coarse_pass_knob() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TVP_COARSE_PASS");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v != 0;
+}
+
 template <typename T>
 cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
     a.coarse = (a.mask_in == nullptr && !per_edge && coarse_knob()) ? 1 : 0;
     const int split = row_fwd_split();
+    if (a.n > 512 && split == 2 && a.coarse && a.mask_out && a.mw == (a.n + 14) / 16 && coarse_pass_knob()) {
+        e = dykstra ? coarse_rows_t<T, true>(a, s) : coarse_rows_t<T, false>(a, s);
+        if (e != cudaSuccess) return e;
+        a.mask_in = a.mask_out;                  // in place: each line reads its words before writing them
+        a.coarse = 0;
+    }
     if (a.n > 512 && split == 2) {               // 1024-sample lines: two warps x 16 samples per lane
         if (dykstra) return row_fwd_w_t<T, 16, 2, false, true>(a, s);
         if (per_edge) return row_fwd_w_t<T, 16, 2, true, false>(a, s);
