@@ -443,9 +443,9 @@ k_row_fwd_w(RowFwdArgs<T> a) {
 // fine kernel then starts from it as a warm start and overwrites the mask.  Kept
 // out of the fine kernel so that the hot PN loop owns the instruction cache.
 // ===========================================================================
-template <typename T, int CPL, bool DYK, int WPB>
+template <typename T, int EF, int CPL, bool DYK, int WPB>
 __global__ void __launch_bounds__(WPB * 32) k_coarse_rows(RowFwdArgs<T> a) {
-    constexpr int EF = 16;                  // fine samples per coarse block (= fine E)
+    // EF: fine samples per coarse block (= the fine kernel's samples per lane)
     constexpr int E = EF * CPL;             // samples per lane here
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = a.n, i0 = lane * E;
@@ -484,12 +484,27 @@ __global__ void __launch_bounds__(WPB * 32) k_coarse_rows(RowFwdArgs<T> a) {
         lc.r = lam * (T(1) / T(EF));
         pn_solve<T, CPL, 32, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active);
         const T xn = shdn<32>(wc[0], 1);
+        if (EF == 16) {
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-            const int j = lane * CPL + q;            // coarse edge j = fine edge 16 j + 15 = word j, bits 30..31
-            const T nx = (q + 1 < CPL) ? wc[(q + 1 < CPL) ? q + 1 : q] : xn;
-            const uint32_t code = (active && j < nc - 1) ? (nx > wc[q] ? CODE_UP : (nx < wc[q] ? CODE_DOWN : 0u)) : 0u;
-            if (j < a.mw) a.mask_out[r * a.mw + j] = code << 30;
+            for (int q = 0; q < CPL; ++q) {
+                const int j = lane * CPL + q;        // coarse edge j = fine edge 16 j + 15 = word j, bits 30..31
+                const T nx = (q + 1 < CPL) ? wc[(q + 1 < CPL) ? q + 1 : q] : xn;
+                const uint32_t code = (active && j < nc - 1) ? (nx > wc[q] ? CODE_UP : (nx < wc[q] ? CODE_DOWN : 0u)) : 0u;
+                if (j < a.mw) a.mask_out[r * a.mw + j] = code << 30;
+            }
+        } else {
+            // coarse edge j = fine edge e = EF (j + 1) - 1: word e / 16, bits 2 (e mod 16);
+            // words are assembled by warp OR-reductions (CPL == 1 here)
+            static_assert(EF == 16 || CPL == 1, "one coarse sample per lane");
+            const int j = lane;
+            const int e = EF * (j + 1) - 1;
+            const uint32_t code = (active && j < nc - 1) ? (xn > wc[0] ? CODE_UP : (xn < wc[0] ? CODE_DOWN : 0u)) : 0u;
+            const int myw = e >> 4;
+            const uint32_t bits = code << (2 * (e & 15));
+            for (int wd = 0; wd < a.mw; ++wd) {
+                const uint32_t word = __reduce_or_sync(FULL, myw == wd ? bits : 0u);
+                if (lane == (wd & 31)) a.mask_out[r * a.mw + wd] = word;
+            }
         }
     }
 }

@@ -111,10 +111,10 @@ static bool coarse_knob() {
 
 // Coarse pre-pass for the long-row geometry (E = 16 fine blocks): writes the initial
 // mask into mask_out, which the fine kernel then reads as its warm start.
-template <typename T, bool DYK>
+template <typename T, int EF, int CPL, bool DYK>
 static cudaError_t coarse_rows_t(const RowFwdArgs<T>& a, cudaStream_t s) {
     constexpr int WPB = 4;
-    auto kern = k_coarse_rows<T, 2, DYK, WPB>;
+    auto kern = k_coarse_rows<T, EF, CPL, DYK, WPB>;
     const int grid = persistent_grid(kern, WPB * 32, 0, (a.nlines + WPB - 1) / WPB);
     kern<<<grid, WPB * 32, 0, s>>>(a);
     count_launch();
@@ -136,12 +136,22 @@ cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStr
     cudaError_t e = cudaSuccess;
     a.coarse = (a.mask_in == nullptr && !per_edge && coarse_knob()) ? 1 : 0;
     const int split = row_fwd_split();
-    if (a.n > 512 && split == 2 && a.coarse && a.mask_out && a.mw == (a.n + 14) / 16 && coarse_pass_knob()) {
-        e = dykstra ? coarse_rows_t<T, true>(a, s) : coarse_rows_t<T, false>(a, s);
+    if (a.coarse && a.mask_out && a.n >= 3 * 4 && coarse_pass_knob()) {
+        // coarse pre-pass with the block size of the fine geometry (E samples per lane)
+        if (a.n > 512 && split == 2) {
+            e = dykstra ? coarse_rows_t<T, 16, 2, true>(a, s) : coarse_rows_t<T, 16, 2, false>(a, s);
+        } else if (a.n > 256 && a.n <= 512 && pick_geo(a.n).E == 16) {
+            // (E <= 8 geometries keep the in-kernel coarse solve: their short loops do
+            // not spill the I-cache, and a separate pass measured slower at C5)
+            e = dykstra ? coarse_rows_t<T, 16, 1, true>(a, s) : coarse_rows_t<T, 16, 1, false>(a, s);
+        } else {
+            goto no_pass;
+        }
         if (e != cudaSuccess) return e;
         a.mask_in = a.mask_out;                  // in place: each line reads its words before writing them
         a.coarse = 0;
     }
+no_pass:
     if (a.n > 512 && split == 2) {               // 1024-sample lines: two warps x 16 samples per lane
         if (dykstra) return row_fwd_w_t<T, 16, 2, false, true>(a, s);
         if (per_edge) return row_fwd_w_t<T, 16, 2, true, false>(a, s);
