@@ -519,7 +519,7 @@ k_col_fwd(ColFwdArgs<T> a) {
     constexpr int LP = line_pitch<E, LPR>();
     extern __shared__ __align__(16) unsigned char smraw_[];
     T* bufA = reinterpret_cast<T*>(smraw_);
-    const int TC = a.TC;
+    constexpr int TC = WPB * (32 / LPR) * (LPR == 32 ? 2 : 1);   // == col_tile<LPR>() of the launcher
     T* bufX = bufA + TC * LP;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
@@ -812,7 +812,7 @@ k_col_bwd(ColBwdArgs<T> a) {
     constexpr int LP = line_pitch<E, LPR>();
     extern __shared__ __align__(16) unsigned char smraw_[];
     T* bufV = reinterpret_cast<T*>(smraw_);
-    const int TC = a.TC;
+    constexpr int TC = WPB * (32 / LPR) * (LPR == 32 ? 2 : 1);   // == col_tile<LPR>() of the launcher
     T* bufB = bufV + TC * LP;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
