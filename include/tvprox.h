@@ -20,7 +20,8 @@
  *  - Outputs are bitwise deterministic run to run (no float atomics; all
  *    reductions are fixed-order).
  *  - In-place operation (x == y, Y == X, grad_y == grad_x) is allowed.
- *  - Lines (1D rows, 2D rows and columns) may have 1 <= n <= tvp_max_line().
+ *  - 1D rows may have 1 <= n <= tvp_max_line_1d(dt); 2D rows and columns
+ *    1 <= H, W <= tvp_max_line(dt).
  */
 #ifndef TVPROX_H_
 #define TVPROX_H_
@@ -51,8 +52,11 @@ typedef enum { TVP_OK = 0, TVP_EINVAL = 1, TVP_EUNSUPPORTED = 2, TVP_ECUDA = 3 }
 #define TVP_ITERS_NONFINITE     (-2)   /* NaN/Inf in the row (or its lam): row set to NaN  */
 #define TVP_ITERS_STALL_FLAG    (1 << 16) /* or-ed into a count: accepted at a rounding-level fixed point */
 
-/* Longest line (1D row length n, 2D W and H) the register-resident solver takes. */
+/* Longest 2D line (W and H) the register-resident solver takes (1024). */
 int64_t tvp_max_line(tvp_dtype_t dt);
+/* Longest 1D row (n): one CTA of up to 16 warps holds the row in registers
+ * ("long 1D signals"): 8192 for TVP_F32, 4096 for TVP_F64. */
+int64_t tvp_max_line_1d(tvp_dtype_t dt);
 
 /* ------------------------------------------------------------------ 1D --- */
 /*
@@ -77,7 +81,7 @@ size_t tv1d_mask_words(int64_t n);                 /* ceil((n-1)/16), 0 if n <= 
  *   row_iters   nullable; int32[batch]: PN iterations, or the TVP_ITERS_ codes.
  * Errors: TVP_EINVAL if y/x NULL (batch > 0), n < 1, batch < 0, stride < n,
  * lam_scalar < 0 or non-finite (SCALAR), lam NULL (other modes), or a 2D
- * mode; TVP_EUNSUPPORTED if n > tvp_max_line(dt).
+ * mode; TVP_EUNSUPPORTED if n > tvp_max_line_1d(dt).
  */
 tvp_status_t tv1d_prox_fwd(tvp_dtype_t dt, const void *y, void *x,
                            int64_t batch, int64_t n, int64_t stride,

@@ -175,7 +175,7 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
     for (int k = 0; k < E; ++k) y[k] -= mean;
     // cold solve: initial bound set from the block-restricted problem (coarse_init);
     // lines held by a full warp or more (short lines converge in 3-5 iterations cold)
-    if (!PE && LPR * WPL >= 32 && coarse && n / E >= 3) {
+    if (!PE && LPR * WPL >= 32 && WPL <= 2 && coarse && n / E >= 3) {
         uint32_t cp, cn;
         coarse_init<T, E, LPR, WPL>(y, lam.r, n, active, C, xb, cp, cn);
         warm_pos |= cp;

@@ -136,6 +136,20 @@ cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStr
     cudaError_t e = cudaSuccess;
     a.coarse = (a.mask_in == nullptr && !per_edge && coarse_knob()) ? 1 : 0;
     const int split = row_fwd_split();
+    if (a.n > 1024) {
+        // long 1D rows (f4): one CTA of WPL warps holds the row in registers, E = 16
+        // (fp32) / 8 (fp64) samples per lane; cold start (the coarse solve is for
+        // <= 2 warps per line)
+        a.coarse = 0;
+        if constexpr (sizeof(T) == 4) {
+            if (a.n <= 2048) return per_edge ? row_fwd_w_t<T, 16, 4, true, false>(a, s) : row_fwd_w_t<T, 16, 4, false, false>(a, s);
+            if (a.n <= 4096) return per_edge ? row_fwd_w_t<T, 16, 8, true, false>(a, s) : row_fwd_w_t<T, 16, 8, false, false>(a, s);
+            return per_edge ? row_fwd_w_t<T, 16, 16, true, false>(a, s) : row_fwd_w_t<T, 16, 16, false, false>(a, s);
+        } else {
+            if (a.n <= 2048) return per_edge ? row_fwd_w_t<T, 8, 8, true, false>(a, s) : row_fwd_w_t<T, 8, 8, false, false>(a, s);
+            return per_edge ? row_fwd_w_t<T, 8, 16, true, false>(a, s) : row_fwd_w_t<T, 8, 16, false, false>(a, s);
+        }
+    }
     if (a.coarse && a.mask_out && a.n >= 3 * 4 && coarse_pass_knob()) {
         // coarse pre-pass with the block size of the fine geometry (E samples per lane)
         if (a.n > 512 && split == 2) {
@@ -226,6 +240,16 @@ cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, 
     cudaError_t e = cudaSuccess;
     // TVP_BWD_SPLIT (A/B): warps per long line; default 2 x 16 samples (measured best for n = 1024)
     static const int bsplit = getenv("TVP_BWD_SPLIT") ? atoi(getenv("TVP_BWD_SPLIT")) : 2;
+    if (a.n > 1024) {                             // long 1D rows (f4): one CTA of WPL warps per row
+        if constexpr (sizeof(T) == 4) {
+            if (a.n <= 2048) return per_edge ? row_bwd_w_t<T, 16, 4, false, true>(a, s) : row_bwd_w_t<T, 16, 4, false, false>(a, s);
+            if (a.n <= 4096) return per_edge ? row_bwd_w_t<T, 16, 8, false, true>(a, s) : row_bwd_w_t<T, 16, 8, false, false>(a, s);
+            return per_edge ? row_bwd_w_t<T, 16, 16, false, true>(a, s) : row_bwd_w_t<T, 16, 16, false, false>(a, s);
+        } else {
+            if (a.n <= 2048) return per_edge ? row_bwd_w_t<T, 8, 8, false, true>(a, s) : row_bwd_w_t<T, 8, 8, false, false>(a, s);
+            return per_edge ? row_bwd_w_t<T, 8, 16, false, true>(a, s) : row_bwd_w_t<T, 8, 16, false, false>(a, s);
+        }
+    }
     if (a.n > 512 && bsplit == 1) {               // A/B: 1 warp x 32 samples per thread
         if (dykstra) return row_bwd_w_t<T, 32, 1, true, false>(a, s);
         if (per_edge) return row_bwd_w_t<T, 32, 1, false, true>(a, s);

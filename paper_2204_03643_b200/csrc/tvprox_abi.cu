@@ -50,6 +50,7 @@ const char* tvp_status_string(tvp_status_t s) {
     }
 }
 int64_t tvp_max_line(tvp_dtype_t dt) { (void)dt; return kMaxLine; }
+int64_t tvp_max_line_1d(tvp_dtype_t dt) { return dt == TVP_F64 ? kMaxLine1DF64 : kMaxLine1DF32; }
 size_t tv1d_mask_words(int64_t n) { return (size_t)mask_words(n); }
 
 size_t tv1d_bwd_workspace_bytes(tvp_dtype_t dt, int64_t batch, tvp_lam_mode_t lm) {
@@ -128,7 +129,7 @@ extern "C" tvp_status_t tv1d_prox_fwd(tvp_dtype_t dt, const void* y, void* x, in
     if (batch == 0) return TVP_OK;
     if (!y || !x) return fail(TVP_EINVAL, "tv1d_prox_fwd: NULL y or x");
     if (lm != TVP_LAM_SCALAR && !lam) return fail(TVP_EINVAL, "tv1d_prox_fwd: NULL lam");
-    if (n > kMaxLine) return fail(TVP_EUNSUPPORTED, "tv1d_prox_fwd: n > tvp_max_line()");
+    if (n > tvp_max_line_1d(dt)) return fail(TVP_EUNSUPPORTED, "tv1d_prox_fwd: n > tvp_max_line_1d()");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     return dt == TVP_F32 ? tv1d_fwd_impl<float>(y, x, batch, n, stride, lam, lm, lam_scalar, mask, row_iters, s)
                          : tv1d_fwd_impl<double>(y, x, batch, n, stride, lam, lm, lam_scalar, mask, row_iters, s);
@@ -148,7 +149,7 @@ extern "C" tvp_status_t tv1d_prox_fwd_warm(tvp_dtype_t dt, const void* y, void* 
     if (batch == 0) return TVP_OK;
     if (!y || !x) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: NULL y or x");
     if (lm != TVP_LAM_SCALAR && !lam) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: NULL lam");
-    if (n > kMaxLine) return fail(TVP_EUNSUPPORTED, "tv1d_prox_fwd_warm: n > tvp_max_line()");
+    if (n > tvp_max_line_1d(dt)) return fail(TVP_EUNSUPPORTED, "tv1d_prox_fwd_warm: n > tvp_max_line_1d()");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     return dt == TVP_F32
                ? tv1d_fwd_impl<float>(y, x, batch, n, stride, lam, lm, lam_scalar, mask_out, row_iters, s, mask_in)
@@ -211,7 +212,7 @@ extern "C" tvp_status_t tv1d_prox_bwd(tvp_dtype_t dt, const void* grad_x, const 
     if (!grad_x || !grad_y) return fail(TVP_EINVAL, "tv1d_prox_bwd: NULL grad_x or grad_y");
     if (n > 1 && !mask) return fail(TVP_EINVAL, "tv1d_prox_bwd: NULL mask");
     if (grad_lam && lm == TVP_LAM_SCALAR && !workspace) return fail(TVP_EINVAL, "tv1d_prox_bwd: NULL workspace");
-    if (n > kMaxLine) return fail(TVP_EUNSUPPORTED, "tv1d_prox_bwd: n > tvp_max_line()");
+    if (n > tvp_max_line_1d(dt)) return fail(TVP_EUNSUPPORTED, "tv1d_prox_bwd: n > tvp_max_line_1d()");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     return dt == TVP_F32 ? tv1d_bwd_impl<float>(grad_x, mask, grad_y, grad_lam, batch, n, stride, lm, workspace, s)
                          : tv1d_bwd_impl<double>(grad_x, mask, grad_y, grad_lam, batch, n, stride, lm, workspace, s);

@@ -124,6 +124,46 @@ def test_per_edge_lambda(tp, n):
     _bwd_compare(tp, y, lam, 2, torch.float32, "f32", n)
 
 
+@pytest.mark.parametrize("n", [1025, 1500, 2048, 2049, 3333, 4096, 6000, 8192])
+@pytest.mark.parametrize("kind", ["normal", "step"])
+def test_forward_long_rows_fp32(tp, n, kind):
+    """f4 (long 1D signals): one CTA of 4-16 warps per row, ragged tails included."""
+    y = workloads.random_rows(9400 + n, 9, n, kind, np.float32)
+    lam = np.random.default_rng(n + 5).uniform(0.05, 2.0, 9)
+    x, mask, it = run_gpu(tp, y, lam.astype(np.float32), torch.float32)
+    check_forward(y, lam.astype(np.float32).astype(np.float64), x, mask, it, "f32")
+
+
+@pytest.mark.parametrize("n", [1025, 2048, 3000, 4096])
+def test_forward_long_rows_fp64(tp, n):
+    y = workloads.random_rows(9500 + n, 6, n, "step", np.float64)
+    lam = np.random.default_rng(n + 6).uniform(0.05, 2.0, 6)
+    x, mask, it = run_gpu(tp, y, lam, torch.float64)
+    check_forward(y, lam, x, mask, it, "f64")
+
+
+@pytest.mark.parametrize("n", [1500, 4096, 8192])
+def test_backward_long_rows(tp, n):
+    y = workloads.random_rows(9600 + n, 8, n, "step", np.float32)
+    lam = np.random.default_rng(n + 7).uniform(0.05, 1.0, 8).astype(np.float32)
+    _bwd_compare(tp, y, lam, 1, torch.float32, "f32", n)
+
+
+@pytest.mark.parametrize("n", [2000, 8192])
+def test_per_edge_lambda_long_rows(tp, n):
+    rng = np.random.default_rng(9700 + n)
+    y = rng.standard_normal((6, n)).astype(np.float32)
+    lam = rng.uniform(0.0, 1.2, (6, n - 1)).astype(np.float32)
+    lam[rng.random(lam.shape) < 0.1] = 0.0
+    _bwd_compare(tp, y, lam, 2, torch.float32, "f32", n)
+
+
+def test_long_row_limit(tp):
+    y = torch.zeros((2, 8193), device="cuda")
+    with pytest.raises(Exception):
+        tp.tv1d_fwd(y, 0.5)
+
+
 def test_c1_fp64_full(tp):
     w = workloads.c1()
     _bwd_compare(tp, w.y, w.lam_scalar, 0, torch.float64, "f64", 11)
