@@ -44,6 +44,23 @@ struct Lam {
 
 template <int E> __device__ __forceinline__ bool bit(uint32_t m, int k) { return (m & (1u << k)) != 0u; }
 
+// m |= b  iff  ug > 0 and au >= thr, as two compares (the second predicated on the
+// first) and one predicated OR -- the ALU pipe is the forward's binding pipe.
+__device__ __forceinline__ void or_if_outward(uint32_t& m, float ug, float au, float thr, uint32_t b) {
+    asm("{\n\t.reg .pred p, q;\n\t"
+        "setp.gt.f32 p, %1, 0f00000000;\n\t"
+        "setp.ge.and.f32 q, %2, %3, p;\n\t"
+        "@q or.b32 %0, %0, %4;\n\t}"
+        : "+r"(m) : "f"(ug), "f"(au), "f"(thr), "r"(b));
+}
+__device__ __forceinline__ void or_if_outward(uint32_t& m, double ug, double au, double thr, uint32_t b) {
+    asm("{\n\t.reg .pred p, q;\n\t"
+        "setp.gt.f64 p, %1, 0d0000000000000000;\n\t"
+        "setp.ge.and.f64 q, %2, %3, p;\n\t"
+        "@q or.b32 %0, %0, %4;\n\t}"
+        : "+r"(m) : "d"(ug), "d"(au), "d"(thr), "r"(b));
+}
+
 // Highest set bit of m below position k, or -1.
 __device__ __forceinline__ int prev_bit(uint32_t m, int k) {
     uint32_t mm = k >= 32 ? m : (m & ((1u << k) - 1u));
@@ -158,7 +175,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                                           : (ynext + unext - u[k]);
                 const T g = xk1 - xk;
                 xk = xk1;
-                if ((fabs(u[k]) >= thr) & (u[k] * g > T(0))) outb |= 1u << k;
+                or_if_outward(outb, u[k] * g, fabs(u[k]), thr, 1u << k);
             }
         }
         const uint32_t nb = keep | outb;
@@ -228,25 +245,33 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         const bool lsmode = C.uany(run && !first && (it + 1 >= kLsAfter));
         bool ok = true, clip = false, chg = false;
         if (!lsmode) {
+            // The tests accumulate non-negative violations on the FMA pipe instead of
+            // predicate logic (the ALU pipe binds this loop):
+            //  * r, A restart at bound edges (r = u_i there, so |r| <= lam_i never
+            //    reads as infeasible and clamp(r) = u_i keeps the bound value);
+            //  * sign test u_i (xhat_{i+1} - xhat_i) >= 0 needs no bound mask: across a
+            //    free edge both samples carry the same segment value bitwise (product 0),
+            //    and pinned edges have u = 0;
+            //  * |q| - q > 0 iff q < 0 and e + |e| > 0 iff e > 0, exactly (no FTZ), and
+            //    a sum of non-negative terms is 0 iff every term is.
+            T vio = T(0), dch = T(0);
 #pragma unroll
             for (int k = 0; k < E; ++k) {
                 const T xh = w[k];
                 const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
                 const T t = xh - y[k];
-                r += t;
-                A += fabs(t);
                 const T lk = lam.at(k);
                 const bool bk = bit<E>(bnd, k);
-                const bool sgn_bad = (u[k] * (xh1 - xh) < T(0)) & !bit<E>(pin, k);
-                const T ar = fabs(r);
-                const bool infeas = ar > fma(slackA, A, lk * slack1);
-                ok = ok & !(bk ? sgn_bad : infeas);
-                chg = chg | (!bk & (r != u[k]));
-                A = bk ? fabs(u[k]) : A;
-                const T un = bk ? u[k] : clampv(r, -lk, lk);
-                r = bk ? u[k] : r;
-                u[k] = un;
+                r = bk ? u[k] : r + t;
+                A = bk ? fabs(u[k]) : A + fabs(t);
+                const T q = u[k] * (xh1 - xh);
+                const T e = fabs(r) - fma(slackA, A, lk * slack1);
+                vio += (fabs(q) - q) + (e + fabs(e));
+                dch += fabs(r - u[k]);
+                u[k] = clampv(r, -lk, lk);
             }
+            ok = vio == T(0);
+            chg = dch != T(0);
         } else {
 #pragma unroll
             for (int k = 0; k < E; ++k) {
