@@ -230,6 +230,7 @@ k_row_fwd(RowFwdArgs<T> a) {
     const int grp = lane / LPR, l = lane % LPR;
     T* bufA = sm + (size_t)warp * NBUF * G * LP;
     T* bufX = DYK ? bufA + G * LP : bufA;
+    uint32_t* mwb = reinterpret_cast<uint32_t*>(sm + (size_t)WPB * NBUF * G * LP) + warp * 32;   // mask words
     const int n = a.n;
     const int64_t ngroups = (a.nlines + G - 1) / G;
     for (int64_t gi = (int64_t)blockIdx.x * WPB + warp; gi < ngroups; gi += (int64_t)gridDim.x * WPB) {
@@ -291,8 +292,29 @@ k_row_fwd(RowFwdArgs<T> a) {
                 if (i < n) bufX[grp * LP + spad(i)] = w[k];
             }
         }
+        // ---- a-8 mask: each lane codes its E edges from registers; the (at most two)
+        // partial words it touches are OR-ed into a warp-private word buffer with
+        // shared-memory atomics (n <= 512 here, so a line has <= 32 words)
+        if (a.mask_out) {
+            if (l < 8 || LPR == 32) mwb[grp * (32 / G) + l] = 0u;
+            const T wnx = shdn<LPR>(w[0], 1);
+            const int e0 = l * E;
+            const int wlo = e0 >> 4;
+            uint32_t clo = 0u, chi = 0u;
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                const int e = e0 + k;
+                const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnx;
+                const bool lz = PE ? !(lam.e[PE ? k : 0] > T(0)) : !(lam.r > T(0));
+                const uint32_t code = (e < n - 1) ? edge_code(w[k], xr, lz) << (2 * (e & 15)) : 0u;
+                if ((e >> 4) == wlo) clo |= code; else chi |= code;
+            }
+            __syncwarp();
+            if (valid && clo) atomicOr(&mwb[grp * (32 / G) + wlo], clo);
+            if (valid && chi) atomicOr(&mwb[grp * (32 / G) + wlo + 1], chi);
+        }
         __syncwarp();
-        // ---- a-8: coalesced store of x (and the Dykstra correction P = A - Z)
+        // ---- a-8: coalesced store of x (and the Dykstra correction P = A - Z) and mask
 #pragma unroll
         for (int j = 0; j < G; ++j) {
             const int64_t rj = r0 + j;
@@ -304,22 +326,7 @@ k_row_fwd(RowFwdArgs<T> a) {
                 d0[i] = xv;
                 if (DYK && d1) d1[i] = bufA[j * LP + spad(i)] - xv;
             }
-            if (a.mask_out) {
-                T lz_line = PE ? T(1) : line_lambda(a.lam, a.lam_mode, a.lam_scalar, rj, a.lines_per_plane, a.C);
-                for (int wd = lane; wd < a.mw; wd += 32) {
-                    uint32_t word = 0;
-#pragma unroll 4
-                    for (int q = 0; q < 16; ++q) {
-                        int e = wd * 16 + q;
-                        if (e < n - 1) {
-                            T le = PE ? __ldg(a.lam + rj * a.stride + e) : lz_line;
-                            word |= edge_code(bufX[j * LP + spad(e)], bufX[j * LP + spad(e + 1)], !(le > T(0)))
-                                    << (2 * q);
-                        }
-                    }
-                    a.mask_out[rj * a.mw + wd] = word;
-                }
-            }
+            if (a.mask_out && lane < a.mw) a.mask_out[rj * a.mw + lane] = mwb[j * (32 / G) + lane];
         }
         if (valid && l == 0) {
             if (a.row_iters) a.row_iters[r] = st;

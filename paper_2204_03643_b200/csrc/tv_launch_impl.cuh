@@ -81,7 +81,7 @@ template <typename T, int E, int LPR, bool PE, bool DYK>
 static cudaError_t row_fwd_t(const RowFwdArgs<T>& a, cudaStream_t s) {
     constexpr int G = 32 / LPR;
     constexpr int LP = line_pitch<E, LPR>();
-    const size_t smem = (size_t)kRowWPB * (DYK ? 2 : 1) * G * LP * sizeof(T);
+    const size_t smem = (size_t)kRowWPB * (DYK ? 2 : 1) * G * LP * sizeof(T) + (size_t)kRowWPB * 32 * 4;
     auto kern = k_row_fwd<T, E, LPR, PE, DYK, kRowWPB>;
     const int64_t groups = (a.nlines + G - 1) / G;
     const int grid = persistent_grid(kern, kRowWPB * 32, smem, (groups + kRowWPB - 1) / kRowWPB);
