@@ -528,6 +528,7 @@ k_col_fwd(ColFwdArgs<T> a) {
     T* bufA = reinterpret_cast<T*>(smraw_);
     constexpr int TC = WPB * (32 / LPR) * (LPR == 32 ? 2 : 1);   // == col_tile<LPR>() of the launcher
     T* bufX = bufA + TC * LP;
+    uint32_t* mwb = reinterpret_cast<uint32_t*>(bufX + TC * LP) + (threadIdx.x >> 5) * 64;   // mask words
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
     const int H = a.H, W = a.W;
@@ -587,6 +588,31 @@ k_col_fwd(ColFwdArgs<T> a) {
                 }
                 if (l == 0 && a.iters_max) atomicMax(a.iters_max, st >= 0 ? (st & 0xffff) : (1 << 20));
             }
+            if (a.mask_out) {
+                // column mask words from registers (as in k_row_fwd): each lane's <= 2
+                // partial words OR-ed into the warp's word buffer, then stored per column
+                uint32_t* gw = mwb + grp * (64 / G);
+                for (int q = l; q < 64 / G; q += LPR) gw[q] = 0u;
+                const T wnx = shdn<LPR>(w[0], 1);
+                const int e0 = l * E;
+                const int wlo = e0 >> 4;
+                const bool lz = !(lamp > T(0));
+                uint32_t clo = 0u, chi = 0u;
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    const int e = e0 + k;
+                    const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnx;
+                    const uint32_t code = (e < H - 1) ? edge_code(w[k], xr, lz) << (2 * (e & 15)) : 0u;
+                    if ((e >> 4) == wlo) clo |= code; else chi |= code;
+                }
+                __syncwarp();
+                if (clo) atomicOr(&gw[wlo], clo);
+                if (chi) atomicOr(&gw[wlo + 1], chi);
+                __syncwarp();
+                if (valid)
+                    for (int q = l; q < a.mw; q += LPR) a.mask_out[(p * W + c0 + c) * a.mw + q] = gw[q];
+                __syncwarp();
+            }
         }
         __syncthreads();
         for (int idx = threadIdx.x; idx < H * TC; idx += nth) {
@@ -595,22 +621,6 @@ k_col_fwd(ColFwdArgs<T> a) {
                 T xv = bufX[c * LP + spad(h)];
                 a.Y[base + (int64_t)h * W + c] = xv;
                 if (a.Qout) a.Qout[base + (int64_t)h * W + c] = bufA[c * LP + spad(h)] - xv;
-            }
-        }
-        if (a.mask_out) {
-            const bool lz = !(lamp > T(0));
-            for (int idx = threadIdx.x; idx < TC * a.mw; idx += nth) {
-                int c = idx / a.mw, wd = idx - c * a.mw;
-                if (c < tcw) {
-                    uint32_t word = 0;
-#pragma unroll 4
-                    for (int q = 0; q < 16; ++q) {
-                        int e = wd * 16 + q;
-                        if (e < H - 1)
-                            word |= edge_code(bufX[c * LP + spad(e)], bufX[c * LP + spad(e + 1)], lz) << (2 * q);
-                    }
-                    a.mask_out[(p * W + c0 + c) * a.mw + wd] = word;
-                }
             }
         }
         __syncthreads();

@@ -196,7 +196,7 @@ static cudaError_t col_fwd_t(ColFwdArgs<T> a, cudaStream_t s) {
     constexpr int LP = line_pitch<E, LPR>();
     constexpr int TC = col_tile<LPR>();
     a.TC = TC;
-    const size_t smem = (size_t)2 * TC * LP * sizeof(T);
+    const size_t smem = (size_t)2 * TC * LP * sizeof(T) + (size_t)kColWPB * 64 * 4;
     auto kern = k_col_fwd<T, E, LPR, kColWPB>;
     const int64_t tiles = a.planes * ((a.W + TC - 1) / TC);
     const int grid = persistent_grid(kern, kColWPB * 32, smem, tiles);
