@@ -133,6 +133,15 @@ __device__ __forceinline__ void mask_decode(const MaskWin<E>& mwin, int e0, uint
     bnd &= m; pos &= m; neg &= m;
 }
 
+// Bits k of an E-edge lane window with k >= nv (edges past the line end, pinned).
+template <int E>
+__device__ __forceinline__ uint32_t pin_tail(int nv) {
+    constexpr uint32_t all = (E >= 32) ? 0xffffffffu : ((1u << (E & 31)) - 1u);
+    if (nv <= 0) return all;
+    if (nv >= E) return 0u;
+    return all & ~((1u << nv) - 1u);
+}
+
 template <int E>
 __device__ __forceinline__ void mask_window(const uint32_t* __restrict__ mw, int nw, int e0,
                                             uint32_t& bnd, uint32_t& pos, uint32_t& neg) {

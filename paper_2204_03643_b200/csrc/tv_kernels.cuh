@@ -633,10 +633,8 @@ __device__ __forceinline__ void bwd_mask_bits(const uint32_t* m, int mw, int n, 
                                               uint32_t& bnd, uint32_t& pos, uint32_t& neg) {
     uint32_t b = 0, p = 0, q = 0;
     if (mw > 0) mask_window<E>(m, mw, l * E, b, p, q);
-#pragma unroll
-    for (int k = 0; k < E; ++k)
-        if (l * E + k >= n - 1) b |= 1u << k;
-    bnd = b; pos = p; neg = q;
+    bnd = b | pin_tail<E>(n - 1 - l * E);
+    pos = p; neg = q;
 }
 
 // ===========================================================================
@@ -788,9 +786,7 @@ k_row_bwd_w(RowBwdArgs<T> a) {
         }
         uint32_t bnd = 0, pos = 0, neg = 0;
         if (a.mw > 0) mask_decode<E>(mc, i0, bnd, pos, neg);
-#pragma unroll
-        for (int k = 0; k < E; ++k)
-            if (i0 + k >= n - 1) bnd |= 1u << k;
+        bnd |= pin_tail<E>(n - 1 - i0);
         T lp = T(0);
         seg_mean_c<T, E, 32, WPL>(v, bnd, pos, neg, C, lp);
         if (PE) {

@@ -505,24 +505,25 @@ __device__ __forceinline__ void seg_mean_c(T (&v)[E], uint32_t bnd, uint32_t pos
     const int fb = __ffs(bnd) - 1;
     const uint32_t firstm = bnd ? (firstb * 2u - 1u) : 0u;
     const T fv = (sf + cs) * rcp_(T(fb + 1 + cc));
-    // pass 3 (reverse): broadcast each segment's mean to its samples
+    // pass 3 (reverse): broadcast each segment's mean to its samples, and the lambda
+    // gradient in edge form, sum_e s_e (mean_L(e) - mean_R(e)): d = x_k - (value to
+    // the right) is exactly 0 inside a segment, so sum_e s_e d_e = sum d - 2 sum_neg d
+    // - sum_bnd d, the last term over edges coded "boundary" (s = 0: lam = 0, pinned).
     T cur = C.template scan_rev<2>(fv, fl);
+    const uint32_t zs = bnd & ~(pos | neg);          // edges with zero sign
+    T sd = T(0), sn = T(0), sz = T(0);
 #pragma unroll
     for (int k = E - 1; k >= 0; --k) {
         T x = bit<E>(bnd, k) ? v[k] : cur;
         x = bit<E>(firstm, k) ? fv : x;
+        const T d = x - cur;
+        sd += d;
+        sn += bit<E>(neg, k) ? d : T(0);
+        if (zs) sz += bit<E>(zs, k) ? d : T(0);
         v[k] = x;
         cur = x;
     }
-    // lambda gradient in edge form
-    const T vn = C.template next<1>(v[0]);
-    T lp = T(0);
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-        const T d = v[k] - ((k + 1 < E) ? v[(k + 1 < E) ? k + 1 : k] : vn);
-        lp += bit<E>(pos, k) ? d : T(0);
-        lp -= bit<E>(neg, k) ? d : T(0);
-    }
+    const T lp = sd - T(2) * sn - sz;
     lam_part += lp;
 }
 
