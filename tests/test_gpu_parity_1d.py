@@ -158,6 +158,20 @@ def test_per_edge_lambda_long_rows(tp, n):
     _bwd_compare(tp, y, lam, 2, torch.float32, "f32", n)
 
 
+@pytest.mark.parametrize("n", [100, 224, 300, 700, 1024, 3000])
+def test_forward_inference_no_mask(tp, n):
+    """need_mask=False (inference): the in-kernel coarse solve replaces the pre-pass."""
+    y = workloads.random_rows(9800 + n, 24, n, "step", np.float32)
+    lam = np.random.default_rng(n + 8).uniform(0.05, 1.5, 24).astype(np.float32)
+    yt = torch.as_tensor(y, device="cuda")
+    x, mask, it = tp.tv1d_fwd(yt, torch.as_tensor(lam, device="cuda"), need_mask=False, want_iters=True)
+    assert mask is None
+    x = x.cpu().numpy().astype(np.float64)
+    assert np.all(it.cpu().numpy() >= 0)
+    x_ref, _, _ = oracle.prox1d_batch(y.astype(np.float64), lam.astype(np.float64), nthreads=8)
+    assert np.abs(x - x_ref).max() <= TOL["f32"] * rng_range(y.astype(np.float64))
+
+
 def test_long_row_limit(tp):
     y = torch.zeros((2, 8193), device="cuda")
     with pytest.raises(Exception):

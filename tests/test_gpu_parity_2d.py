@@ -87,7 +87,8 @@ def run_case(tp, X, lam, mode, K, dtype=torch.float32, dkey="f32", grad_seed=1, 
 
 
 @pytest.mark.parametrize("H,W", [(1, 1), (1, 7), (7, 1), (2, 2), (3, 4), (5, 33), (33, 5), (16, 16),
-                                 (56, 56), (64, 65), (100, 37), (224, 224), (129, 300)])
+                                 (56, 56), (64, 65), (100, 37), (224, 224), (129, 300), (20, 700),
+                                 (700, 20), (9, 1024), (1024, 9)])
 def test_shapes(tp, H, W):
     rng = np.random.default_rng(H * 1000 + W)
     X = rng.standard_normal((2, 2, H, W)).astype(np.float32)
@@ -174,3 +175,18 @@ def test_config_full_size_sampled(tp, cfg):
     for p in picks:
         Yr, _ = oracle.prox2d(Xp[p].astype(np.float64), lamp[p], w.iters)
         assert np.abs(Yg[p] - Yr).max() <= TOL["f32"] * rng
+
+
+@pytest.mark.parametrize("H,W", [(56, 56), (224, 224), (37, 600)])
+def test_inference_no_saved(tp, H, W):
+    """training=False (no saved masks; warm starts from the workspace masks, coarse
+    pre-pass / in-kernel coarse paths) matches the oracle like the training call."""
+    rng = np.random.default_rng(77 + H + W)
+    X = rng.standard_normal((2, 3, H, W)).astype(np.float32)
+    lam = torch.as_tensor(np.array([0.2, 0.6, 1.4], np.float32), device="cuda")
+    Y, saved, _ = tp.tv2d_fwd(torch.as_tensor(X, device="cuda"), lam, 4, training=False)
+    assert saved is None
+    Yr, _ = oracle.prox2d_batch(X.reshape(6, H, W).astype(np.float64),
+                                np.tile([0.2, 0.6, 1.4], 2).astype(np.float64), 4, nthreads=8)
+    err = np.abs(Y.cpu().numpy().reshape(6, H, W).astype(np.float64) - Yr).max()
+    assert err <= TOL["f32"] * rng_range(X.astype(np.float64))
