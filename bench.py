@@ -374,13 +374,15 @@ def run_ours(args):
     bwd_gbs = bwd_bytes / (r["bwd_ms"] * 1e-3) / 1e9
     dom = "fwd" if r["fwd_ms"] >= r["bwd_ms"] else "bwd"
     roof = {
-        "kernel": "k_row_fwd_w<float,16,2> (1D projected-Newton forward, 2 warps/line)" if dom == "fwd"
-        else "k_row_bwd (1D segment-mean backward)",
+        "kernel": "tv1d_prox_fwd = k_coarse_rows (coarse bound set) + k_row_fwd_w<float,16,2> (projected "
+                  "Newton, 2 warps/line)" if dom == "fwd" else "k_row_bwd_w (1D segment-mean backward)",
         "bound": "hbm", "achieved": fwd_gbs if dom == "fwd" else bwd_gbs, "peak": peak, "unit": "GB/s",
         "frac": (fwd_gbs if dom == "fwd" else bwd_gbs) / peak, "peak_source": peak_src,
         "traffic": traffic.get("c2_fwd_bytes_per_launch" if dom == "fwd" else "c2_bwd_bytes_per_launch"),
         "algorithmic_bytes_per_launch": fwd_bytes if dom == "fwd" else bwd_bytes,
         "share_of_step": (r["fwd_ms"] if dom == "fwd" else r["bwd_ms"]) / ms_step,
+        # the forward is issue-bound: pipe utilisation from the ncu capture
+        "pipes_ncu": traffic.get("c2_fwd_pipes" if dom == "fwd" else "c2_bwd_pipes"),
         "other_kernel": {"name": "bwd" if dom == "fwd" else "fwd",
                          "achieved": bwd_gbs if dom == "fwd" else fwd_gbs,
                          "frac": (bwd_gbs if dom == "fwd" else fwd_gbs) / peak,

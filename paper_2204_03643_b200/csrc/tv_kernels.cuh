@@ -150,25 +150,41 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
                                           const Comm<T, LPR, WPL>& C, bool coarse = false,
                                           T* xb = nullptr) {
     const int ll = C.w * LPR + C.l;           // line lane
-    uint32_t pin = 0;
-    bool bad = false;
-    T sum = T(0);
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-        int i = ll * E + k;
-        T lk = lam.at(k);
-        bool pk = (i >= n - 1) || !(lk > T(0));
-        pin |= (pk ? 1u : 0u) << k;
-        if (i < n) {
-            bad = bad || !finite_(y[k]);
-            sum += y[k];
-        }
-        if (i < n - 1) bad = bad || !finite_(lk) || (lk < T(0));
-    }
-    bad = C.any(bad);
     constexpr uint32_t allm = (E == 32) ? 0xffffffffu : ((1u << (E & 31)) - 1u);
-    bool allpin = C.all(pin == allm);
-    sum = C.template sum<8>(sum);
+    uint32_t pin;
+    bool bad, allpin;
+    T sum = T(0);
+    if (PE) {
+        pin = 0;
+        bad = false;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            int i = ll * E + k;
+            T lk = lam.at(k);
+            bool pk = (i >= n - 1) || !(lk > T(0));
+            pin |= (pk ? 1u : 0u) << k;
+            if (i < n) {
+                bad = bad || !finite_(y[k]);
+                sum += y[k];
+            }
+            if (i < n - 1) bad = bad || !finite_(lk) || (lk < T(0));
+        }
+        bad = C.any(bad);
+        allpin = C.all(pin == allm);
+        sum = C.template sum<8>(sum);
+    } else {
+        // one lambda per line: pins are the line tail (or everything at lam = 0); a
+        // non-finite sample makes the line sum non-finite (samples past n are 0), so
+        // the finiteness test is one check of the sum (a finite line whose sum
+        // overflows, |y| ~ 1e38, would also be flagged)
+#pragma unroll
+        for (int k = 0; k < E; ++k) sum += y[k];
+        const bool lpos = lam.r > T(0);
+        pin = pin_tail<E>(n - 1 - ll * E) | (lpos ? 0u : allm);
+        allpin = !lpos || n < 2;
+        sum = C.template sum<8>(sum);
+        bad = !finite_(sum) || (n >= 2 && (!finite_(lam.r) || lam.r < T(0)));
+    }
     bool active = valid && !bad && !allpin;
     T mean = active ? sum / T(n) : T(0);
 #pragma unroll

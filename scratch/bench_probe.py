@@ -43,13 +43,12 @@ def run(tag, sampler, gap, steps=20):
         p.terminate()
     f = [e[0].elapsed_time(e[1]) for e in ev]
     b = [e[1].elapsed_time(e[2]) for e in ev]
-    print("%-22s host-enqueue %.1f ms, wall %.1f ms | fwd %s | bwd %s" % (
-        tag, (h1 - h0) * 1e3, (h2 - h0) * 1e3, " ".join("%.2f" % v for v in f), " ".join("%.2f" % v for v in b)),
-        flush=True)
+    f = np.array(f); b = np.array(b)
+    med = np.median(f)
+    print("%-22s steps %d wall %.1f ms | fwd median %.3f max %.3f outliers(>1.2x) %d | bwd max %.3f" % (
+        tag, steps, (h2 - h0) * 1e3, med, f.max(), int((f > 1.2 * med).sum()), b.max()), flush=True)
 
 
 for rep in range(2):
-    run("no-sampler gap0", False, 0.0)
-    run("no-sampler gap0.3", False, 0.3)
-    run("sampler gap0.3", True, 0.3)
-    run("sampler gap0", True, 0.0)
+    run("no-sampler", False, 0.5, steps=300)
+    run("sampler-100ms", True, 1.0, steps=300)

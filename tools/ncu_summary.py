@@ -26,6 +26,8 @@ KEYS = [
     ("launch__block_size", "block"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("smsp__sass_inst_executed_op_shared_ld.sum", "LDS executed"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe % peak"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe % peak"),
 ]
 STALLS = ["no_instruction", "wait", "long_scoreboard", "short_scoreboard", "branch_resolving",
           "math_pipe_throttle", "barrier", "mio_throttle", "lg_throttle", "not_selected", "dispatch_stall"]
@@ -71,12 +73,15 @@ def main():
              "One capture per kernel (`tools/ncu_capture.sh`, `--clock-control none`, cold L2, serialised).",
              "Durations are ncu's; bench.py's live CUDA-event timings are the reported numbers.", ""]
     traffic = {}
+    pipe_info = {}
     for raw in sorted(glob.glob(os.path.join(src, "%s_*.raw.csv" % tag))):
         name = os.path.basename(raw).replace(".raw.csv", "")
         d = read_raw(raw)
         if not d:
             continue
         s = summarize(d, name)
+        pipe_info[name] = {lab: s[lab][0] for lab in ("issue active %", "ALU pipe % peak", "FMA pipe % peak",
+                                                        "achieved occupancy %") if lab in s}
         lines.append("## %s" % name)
         lines.append("")
         lines.append("`%s`" % s["kernel"][:160])
@@ -108,6 +113,11 @@ def main():
     with open(os.path.join(prof, "%s_ncu_summary.md" % tag), "w") as f:
         f.write("\n".join(lines) + "\n")
     tj = {}
+    for name, pipes in pipe_info.items():
+        if name.endswith("c2_row_fwd"):
+            tj["c2_fwd_pipes"] = pipes
+        elif name.endswith("c2_row_bwd"):
+            tj["c2_bwd_pipes"] = pipes
     for k, v in traffic.items():
         if k.endswith("c2_row_fwd"):
             tj["c2_fwd_bytes_per_launch"] = v
