@@ -64,7 +64,7 @@ __device__ __forceinline__ bool group_any(bool pred) { return !group_all<W>(!pre
 // Reciprocal of a small positive count.  fp32: MUFU.RCP (<= 1 ulp), fp64: IEEE.
 __device__ __forceinline__ float rcp_(float c) {
     float r;
-    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(c));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(c));   // c >= 1 (a count): never subnormal
     return r;
 }
 __device__ __forceinline__ double rcp_(double c) { return 1.0 / c; }

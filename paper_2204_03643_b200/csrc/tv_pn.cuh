@@ -44,6 +44,58 @@ struct Lam {
 
 template <int E> __device__ __forceinline__ bool bit(uint32_t m, int k) { return (m & (1u << k)) != 0u; }
 
+// Predicated accumulate / move (dst only changes where bit b of m is set): keeps the
+// per-sample selects off the ALU pipe (predicated FADD / move instead of FSEL).
+__device__ __forceinline__ void padd2(uint32_t m, uint32_t b, float& a0, float x0, float& a1, float x1) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+        "and.b32 t, %2, %3;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "@p add.f32 %0, %0, %4;\n\t"
+        "@p add.f32 %1, %1, %5;\n\t}"
+        : "+f"(a0), "+f"(a1) : "r"(m), "r"(b), "f"(x0), "f"(x1));
+}
+__device__ __forceinline__ void padd2(uint32_t m, uint32_t b, double& a0, double x0, double& a1, double x1) {
+    if (m & b) { a0 += x0; a1 += x1; }
+}
+
+// Largest E for which the segment pass uses the predicated-move form below (same-box
+// A/B: it wins for the short 2D lines, E = 7, and loses for E = 16 and the coarse
+// E = 2 lines, where the compiler's own select scheduling is better).
+#ifndef TVP_SEG_PTX_MAXE
+#define TVP_SEG_PTX_MAXE 8
+#endif
+// One sample of the lane-local segment pass (P1b) with predicated moves: on a bound
+// edge (bit b of nb) the segment value num / cnt (num itself on the lane's first bound,
+// which still lacks its carry) is stored and the running sums restart.
+__device__ __forceinline__ void seg_step(uint32_t nb, uint32_t fbm, uint32_t b, float num, float cnt, float uk,
+                                         float& w, float& numf, float& ub, float& s, float& c) {
+    asm("{\n\t.reg .pred pb, pf;\n\t.reg .b32 t1, t2;\n\t.reg .f32 r, v;\n\t"
+        "and.b32 t1, %5, %7;\n\t"
+        "setp.ne.u32 pb, t1, 0;\n\t"
+        "and.b32 t2, %6, %7;\n\t"
+        "setp.ne.u32 pf, t2, 0;\n\t"
+        "rcp.approx.ftz.f32 r, %9;\n\t"
+        "mul.f32 v, %8, r;\n\t"
+        "@pf mov.f32 v, %8;\n\t"
+        "@pf mov.f32 %1, %8;\n\t"
+        "@pb mov.f32 %0, v;\n\t"
+        "@pb mov.f32 %2, %10;\n\t"
+        "@pb neg.f32 %3, %10;\n\t"
+        "@pb mov.f32 %4, 0f00000000;\n\t}"
+        : "+f"(w), "+f"(numf), "+f"(ub), "+f"(s), "+f"(c)
+        : "r"(nb), "r"(fbm), "r"(b), "f"(num), "f"(cnt), "f"(uk));
+}
+__device__ __forceinline__ void seg_step(uint32_t nb, uint32_t fbm, uint32_t b, double num, double cnt, double uk,
+                                         double& w, double& numf, double& ub, double& s, double& c) {
+    const bool bk = (nb & b) != 0u, fk = (fbm & b) != 0u;
+    const double val = fk ? num : num * rcp_(cnt);
+    numf = fk ? num : numf;
+    w = bk ? val : w;
+    ub = bk ? uk : ub;
+    s = bk ? -uk : s;
+    c = bk ? 0.0 : c;
+}
+
 // m |= b  iff  ug > 0 and au >= thr, as two compares (the second predicated on the
 // first) and one predicated OR -- the ALU pipe is the forward's binding pipe.
 __device__ __forceinline__ void or_if_outward(uint32_t& m, float ug, float au, float thr, uint32_t b) {
@@ -187,14 +239,18 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             s += y[k];
             cnt += T(1);
             const T num = s + u[k];
-            const bool bk = bit<E>(nb, k);
-            const bool fk = bit<E>(firstb, k);
-            const T val = fk ? num : num * rcp_(cnt);
-            numf = fk ? num : numf;
-            w[k] = bk ? val : w[k];
-            ub = bk ? u[k] : ub;
-            s = bk ? -u[k] : s;
-            cnt = bk ? T(0) : cnt;
+            if (E >= 4 && E <= TVP_SEG_PTX_MAXE) {
+                seg_step(nb, firstb, 1u << k, num, cnt, u[k], w[k], numf, ub, s, cnt);
+            } else {
+                const bool bk = bit<E>(nb, k);
+                const bool fk = bit<E>(firstb, k);
+                const T val = fk ? num : num * rcp_(cnt);
+                numf = fk ? num : numf;
+                w[k] = bk ? val : w[k];
+                ub = bk ? u[k] : ub;
+                s = bk ? -u[k] : s;
+                cnt = bk ? T(0) : cnt;
+            }
         }
         const bool bchg = C.any(nb != bnd);
         // rounding-level fixed point (no change) or 2-cycle of the bound set: stall
@@ -226,9 +282,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             w[k] = v;
             cur = v;
             const T t = v - y[k];
-            const bool tk = bit<E>(tailm, k);
-            rt += tk ? t : T(0);
-            at += tk ? fabs(t) : T(0);
+            padd2(tailm, 1u << k, rt, t, at, fabs(t));
         }
         if (fin) break;
 
