@@ -52,6 +52,12 @@ typedef enum { TVP_OK = 0, TVP_EINVAL = 1, TVP_EUNSUPPORTED = 2, TVP_ECUDA = 3 }
 #define TVP_ITERS_NONFINITE     (-2)   /* NaN/Inf in the row (or its lam): row set to NaN  */
 #define TVP_ITERS_STALL_FLAG    (1 << 16) /* or-ed into a count: accepted at a rounding-level fixed point */
 
+/* Performance switch of the 2D forward: planes with 32 < H, W <= 64
+ * run all K Dykstra passes on chip (one CTA per plane, state in shared memory);
+ * the result is bitwise the staged path's.  Default on (env TVP_FUSED2D=0 turns it
+ * off); returns the previous setting.  Not thread-safe against concurrent calls. */
+int tvp_set_fused2d(int enable);
+
 /* Longest 2D line (W and H) the register-resident solver takes (1024). */
 int64_t tvp_max_line(tvp_dtype_t dt);
 /* Longest 1D row (n): one CTA of up to 16 warps holds the row in registers

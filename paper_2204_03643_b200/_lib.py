@@ -19,7 +19,7 @@ ITERS_NOT_CONVERGED, ITERS_NONFINITE, ITERS_STALL_FLAG = -1, -2, 1 << 16
 
 # every symbol include/tvprox.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "tvp_max_line", "tvp_max_line_1d", "tv1d_mask_words", "tv1d_prox_fwd", "tv1d_prox_fwd_warm", "tv1d_bwd_workspace_bytes",
+    "tvp_max_line", "tvp_max_line_1d", "tvp_set_fused2d", "tv1d_mask_words", "tv1d_prox_fwd", "tv1d_prox_fwd_warm", "tv1d_bwd_workspace_bytes",
     "tv1d_prox_bwd",
     "tv2d_saved_bytes", "tv2d_workspace_bytes", "tv2d_prox_fwd", "tv2d_prox_bwd",
     "tv2d_lines_fwd", "tv2d_lines_workspace_bytes", "tv2d_lines_bwd",
@@ -58,6 +58,8 @@ def load(path: str = LIB_PATH):
         _sig(lib, "tvp_max_line", "argtypes", [i32])
         _sig(lib, "tvp_max_line", "restype", i64)
         _sig(lib, "tvp_max_line_1d", "argtypes", [i32])
+        _sig(lib, "tvp_set_fused2d", "argtypes", [i32])
+        _sig(lib, "tvp_set_fused2d", "restype", i32)
         _sig(lib, "tvp_max_line_1d", "restype", i64)
         _sig(lib, "tv1d_mask_words", "argtypes", [i64])
         _sig(lib, "tv1d_mask_words", "restype", u64)

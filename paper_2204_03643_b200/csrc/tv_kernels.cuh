@@ -906,6 +906,182 @@ k_col_bwd(ColBwdArgs<T> a) {
 }
 
 // ===========================================================================
+// f2: fused on-chip 2D Dykstra forward for small planes (32 < H, W <= 64, e.g. the
+// ResNet 56x56 stage of C3).  One CTA owns a plane: the state Y/Z, P and Q stays in
+// shared memory across all K row and column passes (Alg. 1), HBM sees the
+// input once, the output once and the saved masks; each warp keeps the warm-start
+// bits of the lines it owns in registers from one pass to the next.  Every line
+// is solved by the same solve_line / pn_solve as the staged passes, with the same
+// lane geometry (E samples per lane, 8 lanes per line), so the result is bitwise
+// the staged path's.
+// ===========================================================================
+template <typename T>
+struct PlaneFwdArgs {
+    const T* X;
+    T* Y;
+    const T* lam;
+    int lam_mode;
+    T lam_scalar;
+    int C;
+    int64_t planes;
+    int H, W, K;
+    uint32_t* saved;          // nullable (inference): K row-mask sets then K column-mask sets
+    int mwr, mwc;
+    int32_t* iters_max;       // nullable: 2K entries
+};
+
+template <typename T, int ER, int EC, int WPB>
+__global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) : 1)) k_plane_fwd(PlaneFwdArgs<T> a) {
+    constexpr int LPR = 8, G = 4;                     // 8 lanes per line, 4 lines per warp
+    extern __shared__ __align__(16) unsigned char smraw_[];
+    const int H = a.H, W = a.W, K = a.K;
+    const int PW = W | 1;                             // odd pitch: conflict-free column reads
+    T* ys = reinterpret_cast<T*>(smraw_);
+    T* ps = ys + H * PW;
+    T* qs = ps + H * PW;
+    uint32_t* mwb = reinterpret_cast<uint32_t*>(qs + H * PW) + (threadIdx.x >> 5) * 32;
+    // warm-start bits of every line lane, per orientation: [2][16 tasks][32 lanes] x (up, down)
+    uint32_t* wrp = reinterpret_cast<uint32_t*>(qs + H * PW) + WPB * 32;
+    uint32_t* wrn = wrp + 16 * 32;
+    uint32_t* wcp = wrn + 16 * 32;
+    uint32_t* wcn = wcp + 16 * 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / LPR, l = lane % LPR;
+    const int nth = WPB * 32;
+    const int64_t HW = (int64_t)H * W;
+    const int64_t rset = a.planes * H * a.mwr, cset = a.planes * W * a.mwc;
+    const Comm<T, LPR, 1> Cm{l, 0, nullptr, nullptr};
+    for (int64_t p = blockIdx.x; p < a.planes; p += gridDim.x) {
+        const T lamp = line_lambda(a.lam, a.lam_mode, a.lam_scalar, p, 1, a.C);
+        const bool lz = !(lamp > T(0));
+        for (int i = threadIdx.x; i < H * W; i += nth) {
+            const int h = i / W, c = i - h * W;
+            ys[h * PW + c] = __ldg(a.X + p * HW + i);
+        }
+        __syncthreads();
+        for (int k = 1; k <= K; ++k) {
+            // ---------------- row pass: Z = rowprox(Y + P); P <- (Y + P) - Z
+#pragma unroll 1
+            for (int t = warp; t * G < H; t += WPB) {
+                const int r = t * G + grp;
+                const bool valid = r < H;
+                const uint32_t wp0 = k > 1 ? wrp[t * 32 + lane] : 0u, wn0 = k > 1 ? wrn[t * 32 + lane] : 0u;
+                T y[ER], w[ER], av[ER];
+#pragma unroll
+                for (int q = 0; q < ER; ++q) {
+                    const int i = l * ER + q;
+                    const bool in = valid && i < W;
+                    av[q] = in ? ys[r * PW + i] + (k > 1 ? ps[r * PW + i] : T(0)) : T(0);
+                    y[q] = av[q];
+                }
+                Lam<T, ER, false> lm;
+                lm.r = lamp;
+                const int st = solve_line<T, ER, LPR, 1, false>(y, w, lm, W, valid, wp0, wn0, Cm);
+                // codes of the lane's edges: next pass's warm bits and the saved mask
+                const T wnx = shdn<LPR>(w[0], 1);
+                uint32_t up = 0u, dn = 0u, clo = 0u, chi = 0u;
+                const int e0 = l * ER, wlo = e0 >> 4;
+#pragma unroll
+                for (int q = 0; q < ER; ++q) {
+                    const int e = e0 + q;
+                    const T xr = (q + 1 < ER) ? w[(q + 1 < ER) ? q + 1 : q] : wnx;
+                    const uint32_t code = (e < W - 1) ? edge_code(w[q], xr, lz) : 0u;
+                    up |= (code == CODE_UP ? 1u : 0u) << q;
+                    dn |= (code == CODE_DOWN ? 1u : 0u) << q;
+                    if ((e >> 4) == wlo) clo |= code << (2 * (e & 15)); else chi |= code << (2 * (e & 15));
+                }
+                wrp[t * 32 + lane] = up;
+                wrn[t * 32 + lane] = dn;
+                if (valid) {
+#pragma unroll
+                    for (int q = 0; q < ER; ++q) {
+                        const int i = l * ER + q;
+                        if (i < W) {
+                            ys[r * PW + i] = w[q];
+                            ps[r * PW + i] = av[q] - w[q];
+                        }
+                    }
+                    if (l == 0 && a.iters_max) atomicMax(a.iters_max + 2 * (k - 1), st >= 0 ? (st & 0xffff) : (1 << 20));
+                }
+                if (a.saved) {
+                    uint32_t* gw = mwb + grp * 8;
+                    gw[l] = 0u;
+                    __syncwarp();
+                    if (clo) atomicOr(&gw[wlo], clo);
+                    if (chi) atomicOr(&gw[wlo + 1], chi);
+                    __syncwarp();
+                    if (valid && l < a.mwr)
+                        a.saved[(int64_t)(k - 1) * rset + (p * H + r) * a.mwr + l] = gw[l];
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+            // ---------------- column pass: Y = colprox(Z + Q); Q <- (Z + Q) - Y
+#pragma unroll 1
+            for (int t = warp; t * G < W; t += WPB) {
+                const int c = t * G + grp;
+                const bool valid = c < W;
+                const uint32_t wp0 = k > 1 ? wcp[t * 32 + lane] : 0u, wn0 = k > 1 ? wcn[t * 32 + lane] : 0u;
+                T y[EC], w[EC], bv[EC];
+#pragma unroll
+                for (int q = 0; q < EC; ++q) {
+                    const int h = l * EC + q;
+                    const bool in = valid && h < H;
+                    bv[q] = in ? ys[h * PW + c] + (k > 1 ? qs[h * PW + c] : T(0)) : T(0);
+                    y[q] = bv[q];
+                }
+                Lam<T, EC, false> lm;
+                lm.r = lamp;
+                const int st = solve_line<T, EC, LPR, 1, false>(y, w, lm, H, valid, wp0, wn0, Cm);
+                const T wnx = shdn<LPR>(w[0], 1);
+                uint32_t up = 0u, dn = 0u, clo = 0u, chi = 0u;
+                const int e0 = l * EC, wlo = e0 >> 4;
+#pragma unroll
+                for (int q = 0; q < EC; ++q) {
+                    const int e = e0 + q;
+                    const T xr = (q + 1 < EC) ? w[(q + 1 < EC) ? q + 1 : q] : wnx;
+                    const uint32_t code = (e < H - 1) ? edge_code(w[q], xr, lz) : 0u;
+                    up |= (code == CODE_UP ? 1u : 0u) << q;
+                    dn |= (code == CODE_DOWN ? 1u : 0u) << q;
+                    if ((e >> 4) == wlo) clo |= code << (2 * (e & 15)); else chi |= code << (2 * (e & 15));
+                }
+                wcp[t * 32 + lane] = up;
+                wcn[t * 32 + lane] = dn;
+                if (valid) {
+#pragma unroll
+                    for (int q = 0; q < EC; ++q) {
+                        const int h = l * EC + q;
+                        if (h < H) {
+                            ys[h * PW + c] = w[q];
+                            if (k < K) qs[h * PW + c] = bv[q] - w[q];
+                        }
+                    }
+                    if (l == 0 && a.iters_max)
+                        atomicMax(a.iters_max + 2 * (k - 1) + 1, st >= 0 ? (st & 0xffff) : (1 << 20));
+                }
+                if (a.saved) {
+                    uint32_t* gw = mwb + grp * 8;
+                    gw[l] = 0u;
+                    __syncwarp();
+                    if (clo) atomicOr(&gw[wlo], clo);
+                    if (chi) atomicOr(&gw[wlo + 1], chi);
+                    __syncwarp();
+                    if (valid && l < a.mwc)
+                        a.saved[(int64_t)K * rset + (int64_t)(k - 1) * cset + (p * W + c) * a.mwc + l] = gw[l];
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+        }
+        for (int i = threadIdx.x; i < H * W; i += nth) {
+            const int h = i / W, c = i - h * W;
+            a.Y[p * HW + i] = ys[h * PW + c];
+        }
+        __syncthreads();
+    }
+}
+
+// ===========================================================================
 // Fixed-order lambda-gradient reduction (deterministic, no float atomics).
 // Output q = sum over rep in [0, reps), s in [0, seglen) of
 //   part[rep * rep_stride + q * q_stride + s]

@@ -331,7 +331,41 @@ cudaError_t launch_axpby(const T* x, T* y, T a, T b, int64_t n, cudaStream_t s) 
     return cudaGetLastError();
 }
 
+// f2 fused plane forward (32 < H, W <= 64); E per orientation as in the staged passes
+#ifndef TVP_PLANE_WPB
+#define TVP_PLANE_WPB 8
+#endif
+template <typename T, int ER, int EC>
+static cudaError_t plane_fwd_t(const PlaneFwdArgs<T>& a, cudaStream_t s) {
+    constexpr int WPB = TVP_PLANE_WPB;
+    const int PW = a.W | 1;
+    const size_t smem = (size_t)3 * a.H * PW * sizeof(T) + (size_t)WPB * 32 * 4 + (size_t)4 * 16 * 32 * 4;
+    auto kern = k_plane_fwd<T, ER, EC, WPB>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int dev = 0, sms = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WPB * 32, smem);
+    const int64_t g = std::min<int64_t>(a.planes, (int64_t)sms * std::max(occ, 1));
+    kern<<<(int)std::max<int64_t>(g, 1), WPB * 32, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_plane_fwd(const PlaneFwdArgs<T>& a, cudaStream_t s) {
+    const int er = pick_geo(a.W).E, ec = pick_geo(a.H).E;
+    if (er == 7 && ec == 7) return plane_fwd_t<T, 7, 7>(a, s);
+    if (er == 7) return plane_fwd_t<T, 7, 8>(a, s);
+    if (ec == 7) return plane_fwd_t<T, 8, 7>(a, s);
+    return plane_fwd_t<T, 8, 8>(a, s);
+}
+
 #define TVP_INSTANTIATE(T)                                                                         \
+    template cudaError_t launch_plane_fwd<T>(const PlaneFwdArgs<T>&, cudaStream_t);                \
     template cudaError_t launch_row_fwd<T>(RowFwdArgs<T>, bool, bool, cudaStream_t);        \
     template cudaError_t launch_col_fwd<T>(ColFwdArgs<T>, cudaStream_t);                           \
     template cudaError_t launch_row_bwd<T>(const RowBwdArgs<T>&, bool, bool, cudaStream_t);        \

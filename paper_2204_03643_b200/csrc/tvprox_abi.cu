@@ -4,6 +4,7 @@
 // per-dtype launchers.  No compute happens here; every step runs in kernels.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -15,6 +16,12 @@ namespace tvp {
 static thread_local std::string g_err;
 static thread_local int64_t g_launches = 0;
 void count_launch() { ++g_launches; }
+// f2 fused on-chip 2D path switch (default on; TVP_FUSED2D=0 or tvp_set_fused2d(0) -> staged)
+static bool fused2d_default() {
+    const char* e = getenv("TVP_FUSED2D");
+    return !(e && atoi(e) == 0);
+}
+static bool g_fused2d = fused2d_default();
 }  // namespace tvp
 
 using namespace tvp;
@@ -50,6 +57,11 @@ const char* tvp_status_string(tvp_status_t s) {
     }
 }
 int64_t tvp_max_line(tvp_dtype_t dt) { (void)dt; return kMaxLine; }
+int tvp_set_fused2d(int enable) {
+    const int prev = g_fused2d ? 1 : 0;
+    g_fused2d = enable != 0;
+    return prev;
+}
 int64_t tvp_max_line_1d(tvp_dtype_t dt) { return dt == TVP_F64 ? kMaxLine1DF64 : kMaxLine1DF32; }
 size_t tv1d_mask_words(int64_t n) { return (size_t)mask_words(n); }
 
@@ -245,6 +257,25 @@ static tvp_status_t tv2d_fwd_impl(const void* Xv, void* Yv, int64_t N, int64_t C
     if (line_iters) {
         cudaError_t e = cudaMemsetAsync(line_iters, 0, sizeof(int32_t) * 2 * K, s);
         if (e != cudaSuccess) return cuda_status(e, "tv2d_prox_fwd");
+    }
+    if (g_fused2d && plane_fwd_supported(H, W)) {
+        // f2: the whole plane stays on chip for all K passes (no Z/P/Q workspace traffic)
+        PlaneFwdArgs<T> f{};
+        f.X = X;
+        f.Y = Y;
+        f.lam = static_cast<const T*>(lam);
+        f.lam_mode = (int)lm;
+        f.lam_scalar = (T)lam_scalar;
+        f.C = (int)(C > 0 ? C : 1);
+        f.planes = planes;
+        f.H = (int)H;
+        f.W = (int)W;
+        f.K = K;
+        f.saved = sv;
+        f.mwr = (int)mwr;
+        f.mwc = (int)mwc;
+        f.iters_max = line_iters;
+        return cuda_status(launch_plane_fwd<T>(f, s), "tv2d_prox_fwd(fused)");
     }
     for (int k = 1; k <= K; ++k) {
         // ---- row pass (Alg. 1 lines 3-6): Z = rowprox(Y + P); P <- (Y + P) - Z

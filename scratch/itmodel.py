@@ -130,3 +130,26 @@ def run2():
         its = np.array(its)
         print("m=%d inner=%s fine mean %.2f p99 %d max %d | coarse mean %.2f max %d | inner mean %.2f" % (
             m, inner, its.mean(), np.percentile(its, 99), its.max(), np.mean(cits), max(cits), np.mean(c2its)))
+
+
+def run3():
+    """How many fine iterations from perturbed exact bound sets (what a better init could buy)."""
+    w = workloads.c2(batch=128)
+    for shift in (0, 1, 2, 4, 8):
+        its = []
+        for b in range(128):
+            y = w.y[b].astype(np.float64)
+            lam = float(w.lam[b])
+            x = oracle.prox1d(y, lam)
+            d = np.diff(x)
+            n = len(y)
+            pos = np.zeros(n, bool); neg = np.zeros(n, bool)
+            rng = np.random.default_rng(b)
+            for e in np.flatnonzero(np.abs(d) > 0):
+                e2 = int(np.clip(e + rng.integers(-shift, shift + 1), 0, n - 2))
+                if d[e] > 0: pos[e2] = True
+                else: neg[e2] = True
+            _, it = pn(y, lam, pos, neg)
+            its.append(it)
+        its = np.array(its)
+        print("exact jumps shifted by <= %d: fine iters mean %.2f max %d" % (shift, its.mean(), its.max()))

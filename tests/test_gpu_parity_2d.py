@@ -190,3 +190,38 @@ def test_inference_no_saved(tp, H, W):
                                 np.tile([0.2, 0.6, 1.4], 2).astype(np.float64), 4, nthreads=8)
     err = np.abs(Y.cpu().numpy().reshape(6, H, W).astype(np.float64) - Yr).max()
     assert err <= TOL["f32"] * rng_range(X.astype(np.float64))
+
+
+@pytest.mark.parametrize("H,W,K,mode,dt", [(56, 56, 4, "channel", "f32"), (33, 64, 3, "scalar", "f32"),
+                                            (64, 40, 2, "plane", "f32"), (50, 61, 1, "channel", "f32"),
+                                            (56, 56, 4, "channel", "f64"), (64, 64, 5, "scalar", "f32")])
+def test_fused_plane_matches_staged_bitwise(tp, H, W, K, mode, dt):
+    """f2: the on-chip plane kernel gives bitwise the staged passes' output, saved masks
+    and iteration counts (same line solver, same lane geometry), and matches the oracle."""
+    from paper_2204_03643_b200 import _lib
+    lib = _lib.load()
+    dtype = torch.float32 if dt == "f32" else torch.float64
+    N, C = 3, 2
+    rng = np.random.default_rng(H * 7 + W + K)
+    X = np.maximum(rng.standard_normal((N, C, H, W)), 0).astype(np.float32 if dt == "f32" else np.float64)
+    lam = {"scalar": 0.45, "channel": [0.1, 0.8], "plane": list(rng.uniform(0.05, 1.2, N * C))}[mode]
+    Xt = torch.as_tensor(X, device="cuda")
+    lt = lam if mode == "scalar" else torch.as_tensor(np.asarray(lam), dtype=dtype, device="cuda")
+    outs = []
+    prev = lib.tvp_set_fused2d(1)
+    try:
+        for fused in (1, 0):
+            lib.tvp_set_fused2d(fused)
+            Y, saved, it = tp.tv2d_fwd(Xt, lt, K, training=True, want_iters=True)
+            torch.cuda.synchronize()
+            outs.append((Y.cpu().numpy(), saved.cpu().numpy(), it.cpu().numpy()))
+    finally:
+        lib.tvp_set_fused2d(prev)
+    (Yf, sf, itf), (Ys, ss, its) = outs
+    assert np.array_equal(Yf.view(np.uint8), Ys.view(np.uint8)), "fused != staged output"
+    assert np.array_equal(sf, ss), "fused != staged saved masks"
+    assert np.array_equal(itf, its)
+    lamp = plane_lams(lam, mode, N, C)
+    Yr, _ = oracle.prox2d_batch(X.reshape(N * C, H, W).astype(np.float64), lamp, K, nthreads=8)
+    err = np.abs(Yf.reshape(N * C, H, W).astype(np.float64) - Yr).max()
+    assert err <= TOL[dt] * rng_range(X.astype(np.float64))
