@@ -532,6 +532,89 @@ __global__ void __launch_bounds__(WPB * 32) k_coarse_rows(RowFwdArgs<T> a) {
     }
 }
 
+// Two lines per warp (512 < n <= 1024, blocks of 16): each lane loads 32 samples of
+// each line (two blocks), the 64 block means of a line are regrouped by shuffles onto
+// 16 lanes x 4, and the two coarse lines are solved side by side (16-lane groups), so
+// the per-iteration scan / vote cost is shared by two lines.
+template <typename T, bool DYK, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_coarse_rows2(RowFwdArgs<T> a) {
+    constexpr int EF = 16, E = 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane >> 4, l = lane & 15;
+    const int n = a.n, i0 = lane * E;
+    const int nc = n / EF;
+    const bool vec = ((a.stride & 3) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(a.src0) |
+                       reinterpret_cast<uintptr_t>(DYK && a.src1 ? a.src1 : a.src0)) & 15) == 0;
+    const Comm<T, 16, 1> C{l, 0, nullptr, nullptr};
+    const int64_t npairs = (a.nlines + 1) / 2;
+    for (int64_t pr = (int64_t)blockIdx.x * WPB + warp; pr < npairs; pr += (int64_t)gridDim.x * WPB) {
+        T bm[2][2];                        // [line of the pair][block] means of this lane's 32 samples
+        bool bad[2] = {false, false};
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int64_t r = 2 * pr + j;
+            T v[E];
+            if (r < a.nlines) {
+                ld_contig<T, E>(a.src0 + r * a.stride, i0, n, vec, v);
+                if (DYK && a.src1) {
+                    T p[E];
+                    ld_contig<T, E>(a.src1 + r * a.stride, i0, n, vec, p);
+#pragma unroll
+                    for (int k = 0; k < E; ++k) v[k] += p[k];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < E; ++k) v[k] = T(0);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                T sm = T(0);
+#pragma unroll
+                for (int k = 0; k < EF; ++k) {
+                    sm += v[q * EF + k];
+                    bad[j] = bad[j] || !finite_(v[q * EF + k]);
+                }
+                bm[j][q] = (2 * lane + q < nc) ? sm * (T(1) / T(EF)) : T(0);
+            }
+        }
+        // regroup: lane (grp, l) takes blocks 4l..4l+3 of line grp (from lanes 2l, 2l+1)
+        T yc[4], uc[4], wc[4];
+        {
+            const int s0 = 2 * l, s1 = 2 * l + 1;
+            const T a00 = __shfl_sync(FULL, bm[0][0], s0), a01 = __shfl_sync(FULL, bm[0][1], s0);
+            const T a10 = __shfl_sync(FULL, bm[0][0], s1), a11 = __shfl_sync(FULL, bm[0][1], s1);
+            const T b00 = __shfl_sync(FULL, bm[1][0], s0), b01 = __shfl_sync(FULL, bm[1][1], s0);
+            const T b10 = __shfl_sync(FULL, bm[1][0], s1), b11 = __shfl_sync(FULL, bm[1][1], s1);
+            yc[0] = grp ? b00 : a00;
+            yc[1] = grp ? b01 : a01;
+            yc[2] = grp ? b10 : a10;
+            yc[3] = grp ? b11 : a11;
+        }
+        const bool anybad0 = __any_sync(FULL, bad[0]), anybad1 = __any_sync(FULL, bad[1]);
+        const int64_t r = 2 * pr + grp;
+        const bool rvalid = r < a.nlines;
+        const T lam = rvalid ? line_lambda(a.lam, a.lam_mode, a.lam_scalar, r, a.lines_per_plane, a.C) : T(0);
+        const bool active = rvalid && !(grp ? anybad1 : anybad0) && lam > T(0) && nc >= 3;
+        uint32_t pinc = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pinc |= (4 * l + q >= nc - 1) ? (1u << q) : 0u;
+        Lam<T, 4, false> lc;
+        lc.r = lam * (T(1) / T(EF));
+        pn_solve<T, 4, 16, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active);
+        const T xn = shdn<16>(wc[0], 1);
+        if (rvalid) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = 4 * l + q;            // coarse edge j = fine edge 16 j + 15 = word j, bits 30..31
+                const T nx = (q + 1 < 4) ? wc[(q + 1 < 4) ? q + 1 : q] : xn;
+                const uint32_t code = (active && j < nc - 1) ? (nx > wc[q] ? CODE_UP : (nx < wc[q] ? CODE_DOWN : 0u)) : 0u;
+                if (j < a.mw) a.mask_out[r * a.mw + j] = code << 30;
+            }
+        }
+    }
+}
+
 // ===========================================================================
 // Column forward: Dykstra column pass (tile of TC columns of one plane).
 // ===========================================================================

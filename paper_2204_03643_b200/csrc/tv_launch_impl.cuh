@@ -121,14 +121,26 @@ static cudaError_t coarse_rows_t(const RowFwdArgs<T>& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// TVP_COARSE_PASS=0 keeps the coarse solve inside the long-row forward kernel (A/B).
-static bool coarse_pass_knob() {
+template <typename T, bool DYK>
+static cudaError_t coarse_rows2_t(const RowFwdArgs<T>& a, cudaStream_t s) {
+    constexpr int WPB = 4;
+    auto kern = k_coarse_rows2<T, DYK, WPB>;
+    const int64_t pairs = (a.nlines + 1) / 2;
+    const int grid = persistent_grid(kern, WPB * 32, 0, (pairs + WPB - 1) / WPB);
+    kern<<<grid, WPB * 32, 0, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// TVP_COARSE_PASS=0 keeps the coarse solve inside the long-row forward kernel (A/B);
+// TVP_COARSE_PASS=1 one line per warp, 2 (default) two lines per warp.
+static int coarse_pass_knob() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TVP_COARSE_PASS");
-        v = (e && atoi(e) == 0) ? 0 : 1;
+        v = e ? atoi(e) : 2;
     }
-    return v != 0;
+    return v;
 }
 
 template <typename T>
@@ -153,7 +165,10 @@ cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStr
     if (a.coarse && a.mask_out && a.n >= 3 * 4 && coarse_pass_knob()) {
         // coarse pre-pass with the block size of the fine geometry (E samples per lane)
         if (a.n > 512 && split == 2) {
-            e = dykstra ? coarse_rows_t<T, 16, 2, true>(a, s) : coarse_rows_t<T, 16, 2, false>(a, s);
+            if (coarse_pass_knob() == 2)
+                e = dykstra ? coarse_rows2_t<T, true>(a, s) : coarse_rows2_t<T, false>(a, s);
+            else
+                e = dykstra ? coarse_rows_t<T, 16, 2, true>(a, s) : coarse_rows_t<T, 16, 2, false>(a, s);
         } else if (a.n > 256 && a.n <= 512 && pick_geo(a.n).E == 16) {
             // (E <= 8 geometries keep the in-kernel coarse solve: their short loops do
             // not spill the I-cache, and a separate pass measured slower at C5)
