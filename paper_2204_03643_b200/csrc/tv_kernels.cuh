@@ -1164,6 +1164,110 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
     }
 }
 
+// f2 backward: reverse mode through the K passes (a-14) with the two adjoint planes
+// A (= Ybar = Pbar) and B (= Zbar = Qbar) in shared memory: init A = G, B = 0; for
+// k = K..1: column adjoint B <- B + colsegmean_k(A - B), row adjoint A <- Pbar +
+// rowsegmean_k(B - Pbar) with Pbar = A (0 at k = K).  Same per-line seg_mean calls,
+// geometry and lambda partial slots as k_col_bwd / k_row_bwd (bitwise equal).
+template <typename T>
+struct PlaneBwdArgs {
+    const T* G;
+    T* GX;
+    const uint32_t* saved;
+    int64_t planes;
+    int H, W, K;
+    int mwr, mwc;
+    T* lampart;               // nullable: [plane][k][H + W] partials
+};
+
+template <typename T, int ER, int EC, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_plane_bwd(PlaneBwdArgs<T> a) {
+    constexpr int LPR = 8, G = 4;
+    extern __shared__ __align__(16) unsigned char smraw_[];
+    const int H = a.H, W = a.W, K = a.K;
+    const int PW = W | 1;
+    T* As = reinterpret_cast<T*>(smraw_);
+    T* Bs = As + H * PW;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / LPR, l = lane % LPR;
+    const int nth = WPB * 32;
+    const int64_t HW = (int64_t)H * W;
+    const int64_t rset = a.planes * H * a.mwr, cset = a.planes * W * a.mwc;
+    const int64_t HW2 = H + W;
+    for (int64_t p = blockIdx.x; p < a.planes; p += gridDim.x) {
+        for (int i = threadIdx.x; i < H * W; i += nth) {
+            const int h = i / W, c = i - h * W;
+            As[h * PW + c] = __ldg(a.G + p * HW + i);
+        }
+        __syncthreads();
+        for (int k = K; k >= 1; --k) {
+            // ---- column adjoint: r = A - B; B <- B + colsegmean_k(r)
+#pragma unroll 1
+            for (int t = warp; t * G < W; t += WPB) {
+                const int c = t * G + grp;
+                const bool valid = c < W;
+                T v[EC], bv[EC];
+#pragma unroll
+                for (int q = 0; q < EC; ++q) {
+                    const int h = l * EC + q;
+                    const bool in = valid && h < H;
+                    bv[q] = (in && k < K) ? Bs[h * PW + c] : T(0);
+                    v[q] = (in ? As[h * PW + c] : T(0)) - bv[q];
+                }
+                uint32_t bnd, pos, neg;
+                bwd_mask_bits<EC>(a.saved + (int64_t)K * rset + (int64_t)(k - 1) * cset + (p * W + (valid ? c : 0)) * a.mwc,
+                                  a.mwc, H, l, bnd, pos, neg);
+                T lp = T(0);
+                seg_mean<T, EC, LPR>(v, bnd, pos, neg, l, lp);
+                lp = group_sum<LPR>(lp);
+                if (valid) {
+                    if (l == 0 && a.lampart) a.lampart[p * K * HW2 + (k - 1) * HW2 + H + c] = lp;
+#pragma unroll
+                    for (int q = 0; q < EC; ++q) {
+                        const int h = l * EC + q;
+                        if (h < H) Bs[h * PW + c] = bv[q] + v[q];
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- row adjoint: r = B - Pbar; A <- Pbar + rowsegmean_k(r)
+#pragma unroll 1
+            for (int t = warp; t * G < H; t += WPB) {
+                const int r = t * G + grp;
+                const bool valid = r < H;
+                T v[ER], pv[ER];
+#pragma unroll
+                for (int q = 0; q < ER; ++q) {
+                    const int i = l * ER + q;
+                    const bool in = valid && i < W;
+                    pv[q] = (in && k < K) ? As[r * PW + i] : T(0);
+                    v[q] = (in ? Bs[r * PW + i] : T(0)) - pv[q];
+                }
+                uint32_t bnd, pos, neg;
+                bwd_mask_bits<ER>(a.saved + (int64_t)(k - 1) * rset + (p * H + (valid ? r : 0)) * a.mwr, a.mwr, W, l,
+                                  bnd, pos, neg);
+                T lp = T(0);
+                seg_mean<T, ER, LPR>(v, bnd, pos, neg, l, lp);
+                lp = group_sum<LPR>(lp);
+                if (valid) {
+                    if (l == 0 && a.lampart) a.lampart[p * K * HW2 + (k - 1) * HW2 + r] = lp;
+#pragma unroll
+                    for (int q = 0; q < ER; ++q) {
+                        const int i = l * ER + q;
+                        if (i < W) As[r * PW + i] = pv[q] + v[q];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        for (int i = threadIdx.x; i < H * W; i += nth) {
+            const int h = i / W, c = i - h * W;
+            a.GX[p * HW + i] = As[h * PW + c];
+        }
+        __syncthreads();
+    }
+}
+
 // ===========================================================================
 // Fixed-order lambda-gradient reduction (deterministic, no float atomics).
 // Output q = sum over rep in [0, reps), s in [0, seglen) of

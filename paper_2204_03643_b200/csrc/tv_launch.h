@@ -12,6 +12,7 @@ template <typename T> struct RowBwdArgs;
 template <typename T> struct ColBwdArgs;
 template <typename T> struct LamReduceArgs;
 template <typename T> struct PlaneFwdArgs;
+template <typename T> struct PlaneBwdArgs;
 
 // (E samples per lane, LPR lanes per line) chosen for a line length n.
 struct Geo { int E, LPR; };
@@ -43,6 +44,7 @@ inline int lam_chunks(int64_t total, int64_t nout) {
 template <typename T> cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s);
 template <typename T> cudaError_t launch_col_fwd(ColFwdArgs<T> a, cudaStream_t s);
 template <typename T> cudaError_t launch_plane_fwd(const PlaneFwdArgs<T>& a, cudaStream_t s);
+template <typename T> cudaError_t launch_plane_bwd(const PlaneBwdArgs<T>& a, cudaStream_t s);
 inline bool plane_fwd_supported(int64_t H, int64_t W) { return H > 32 && H <= 64 && W > 32 && W <= 64; }
 template <typename T> cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s);
 template <typename T> cudaError_t launch_col_bwd(ColBwdArgs<T> a, cudaStream_t s);

@@ -379,8 +379,38 @@ cudaError_t launch_plane_fwd(const PlaneFwdArgs<T>& a, cudaStream_t s) {
     return plane_fwd_t<T, 8, 8>(a, s);
 }
 
+template <typename T, int ER, int EC>
+static cudaError_t plane_bwd_t(const PlaneBwdArgs<T>& a, cudaStream_t s) {
+    constexpr int WPB = TVP_PLANE_WPB;
+    const int PW = a.W | 1;
+    const size_t smem = (size_t)2 * a.H * PW * sizeof(T);
+    auto kern = k_plane_bwd<T, ER, EC, WPB>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int dev = 0, sms = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WPB * 32, smem);
+    const int64_t g = std::min<int64_t>(a.planes, (int64_t)sms * std::max(occ, 1));
+    kern<<<(int)std::max<int64_t>(g, 1), WPB * 32, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_plane_bwd(const PlaneBwdArgs<T>& a, cudaStream_t s) {
+    const int er = pick_geo(a.W).E, ec = pick_geo(a.H).E;
+    if (er == 7 && ec == 7) return plane_bwd_t<T, 7, 7>(a, s);
+    if (er == 7) return plane_bwd_t<T, 7, 8>(a, s);
+    if (ec == 7) return plane_bwd_t<T, 8, 7>(a, s);
+    return plane_bwd_t<T, 8, 8>(a, s);
+}
+
 #define TVP_INSTANTIATE(T)                                                                         \
     template cudaError_t launch_plane_fwd<T>(const PlaneFwdArgs<T>&, cudaStream_t);                \
+    template cudaError_t launch_plane_bwd<T>(const PlaneBwdArgs<T>&, cudaStream_t);                \
     template cudaError_t launch_row_fwd<T>(RowFwdArgs<T>, bool, bool, cudaStream_t);        \
     template cudaError_t launch_col_fwd<T>(ColFwdArgs<T>, cudaStream_t);                           \
     template cudaError_t launch_row_bwd<T>(const RowBwdArgs<T>&, bool, bool, cudaStream_t);        \

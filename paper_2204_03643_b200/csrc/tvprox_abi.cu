@@ -353,7 +353,23 @@ static tvp_status_t tv2d_bwd_impl(const void* GYv, const void* saved, void* GXv,
     const T* G = static_cast<const T*>(GYv);
     T* GX = static_cast<T*>(GXv);
     const int64_t HW2 = H + W;
-    for (int k = K; k >= 1; --k) {
+    if (g_fused2d && plane_fwd_supported(H, W)) {
+        // f2: both adjoint planes stay on chip through all 2K adjoint passes
+        PlaneBwdArgs<T> f{};
+        f.G = G;
+        f.GX = GX;
+        f.saved = sv;
+        f.planes = planes;
+        f.H = (int)H;
+        f.W = (int)W;
+        f.K = K;
+        f.mwr = (int)mwr;
+        f.mwc = (int)mwc;
+        f.lampart = glam ? lampart : nullptr;
+        cudaError_t e = launch_plane_bwd<T>(f, s);
+        if (e != cudaSuccess) return cuda_status(e, "tv2d_prox_bwd(fused)");
+    }
+    for (int k = K; k >= 1 && !(g_fused2d && plane_fwd_supported(H, W)); --k) {
         // ---- column adjoint: r = A - B; B <- B + colsegmean_k(r)   (A = G at k = K, B = 0)
         ColBwdArgs<T> c{};
         c.A = (k == K) ? G : GX;

@@ -218,6 +218,21 @@ def test_fused_plane_matches_staged_bitwise(tp, H, W, K, mode, dt):
     finally:
         lib.tvp_set_fused2d(prev)
     (Yf, sf, itf), (Ys, ss, its) = outs
+    # backward (f2 adjoint planes on chip vs the staged adjoint passes) on the same saved masks
+    mode_id = {"scalar": 0, "channel": 3, "plane": 4}[mode]
+    G = torch.as_tensor(rng.standard_normal(X.shape), dtype=dtype, device="cuda")
+    sv = torch.as_tensor(sf, device="cuda")
+    bouts = []
+    try:
+        for fused in (1, 0):
+            lib.tvp_set_fused2d(fused)
+            GX, gl = tp.tv2d_bwd(G, sv, mode_id, K, want_lam=True)
+            torch.cuda.synchronize()
+            bouts.append((GX.cpu().numpy(), gl.cpu().numpy()))
+    finally:
+        lib.tvp_set_fused2d(prev)
+    assert np.array_equal(bouts[0][0].view(np.uint8), bouts[1][0].view(np.uint8)), "fused != staged grad_X"
+    assert np.array_equal(bouts[0][1].view(np.uint8), bouts[1][1].view(np.uint8)), "fused != staged grad_lam"
     assert np.array_equal(Yf.view(np.uint8), Ys.view(np.uint8)), "fused != staged output"
     assert np.array_equal(sf, ss), "fused != staged saved masks"
     assert np.array_equal(itf, its)
