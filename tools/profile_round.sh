@@ -12,4 +12,6 @@ bash tools/ncu_capture.sh k_row_fwd c5 $D/${T}_c5_row_fwd
 bash tools/ncu_capture.sh k_col_fwd c5 $D/${T}_c5_col_fwd
 bash tools/ncu_capture.sh k_row_bwd c5 $D/${T}_c5_row_bwd
 bash tools/ncu_capture.sh k_col_bwd c5 $D/${T}_c5_col_bwd
+bash tools/ncu_capture.sh k_plane_fwd c3 $D/${T}_c3_plane_fwd
+bash tools/ncu_capture.sh k_plane_bwd c3 $D/${T}_c3_plane_bwd
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $D/launches_${T}.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $D/launches_bench.log 2>&1
