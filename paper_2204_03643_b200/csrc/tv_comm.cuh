@@ -11,7 +11,7 @@
 
 namespace tvp {
 
-constexpr int kCommSlots = 12;
+constexpr int kCommSlots = 16;
 
 template <typename T, int LPR, int WPL>
 struct Comm {

@@ -171,7 +171,17 @@ __device__ __forceinline__ T seg_scan_rev(T v, bool f, int l) {
 
 // Iterations after which a line switches from projected full Newton steps to the
 // projected Armijo line search (DESIGN.md a-7).
-constexpr int kLsAfter = 12;
+#ifndef TVP_LS_AFTER
+#define TVP_LS_AFTER 12
+#endif
+constexpr int kLsAfter = TVP_LS_AFTER;
+// f3: TVP_LS_PARALLEL=1 replaces the sequential backtracking by a parallel
+// step search -- four step sizes alpha, alpha/2, alpha/4, alpha/8 evaluated in one
+// fused pass with one reduction, the largest Armijo-accepted one taken (P:188 compares
+// the two; measured in DESIGN.md section 10).
+#ifndef TVP_LS_PARALLEL
+#define TVP_LS_PARALLEL 0
+#endif
 
 template <typename T> __device__ __forceinline__ T big_();
 template <> __device__ __forceinline__ float big_<float>() { return 3.0e38f; }
@@ -378,7 +388,84 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             uchg = chg || first;
         }
         bool pending = lsmode && run && !fast;
-        if (C.uany(pending)) {
+        if (TVP_LS_PARALLEL && C.uany(pending)) {
+            constexpr int NA = 4;
+            T abase = T(1), alpha = T(0);
+            bool accepted = false, lchg = false;
+            for (int round = 0; round < 8; ++round) {
+                if (!C.uany(pending)) break;
+                const T lkl = lam.at(E - 1);
+                T dprev[NA];
+#pragma unroll
+                for (int j = 0; j < NA; ++j) {
+                    const T aj = abase * T(1.0 / (1 << j));
+                    const T dlast = bit<E>(bnd, E - 1) ? T(0)
+                                                       : clampv(u[E - 1] + aj * (w[E - 1] - u[E - 1]), -lkl, lkl) - u[E - 1];
+                    dprev[j] = (j == 0) ? C.template prev<12>(dlast)
+                             : (j == 1) ? C.template prev<13>(dlast)
+                             : (j == 2) ? C.template prev<14>(dlast) : C.template prev<15>(dlast);
+                }
+                T F[NA], Gs[NA];
+                bool ch[NA];
+#pragma unroll
+                for (int j = 0; j < NA; ++j) { F[j] = T(0); Gs[j] = T(0); ch[j] = false; }
+                T x0 = y[0] + u[0] - uprev;
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    const T lk = lam.at(k);
+                    const T dk = bit<E>(bnd, k) ? T(0) : (w[k] - u[k]);
+                    const T x1 = (k + 1 < E) ? (y[(k + 1 < E) ? k + 1 : k] + u[(k + 1 < E) ? k + 1 : k] - u[k])
+                                             : (ynext + unext - u[k]);
+                    const T g = x1 - x0;
+#pragma unroll
+                    for (int j = 0; j < NA; ++j) {
+                        const T aj = abase * T(1.0 / (1 << j));
+                        const T du = clampv(u[k] + aj * dk, -lk, lk) - u[k];
+                        const T dl = du - dprev[j];
+                        F[j] = fma(dl, T(2) * x0 + dl, F[j]);
+                        Gs[j] = fma(g, du, Gs[j]);
+                        ch[j] = ch[j] | (du != T(0));
+                        dprev[j] = du;
+                    }
+                    x0 = x1;
+                }
+                T z = T(0);
+                C.template sum3<7>(F[0], F[1], F[2]);
+                C.template sum3<9>(F[3], Gs[0], Gs[1]);
+                C.template sum3<11>(Gs[2], Gs[3], z);
+                bool chj[NA];
+#pragma unroll
+                for (int j = 0; j < NA; ++j) chj[j] = C.any(ch[j]);
+                if (pending) {
+#pragma unroll
+                    for (int j = NA - 1; j >= 0; --j) {     // keep the largest accepted alpha
+                        const T gain = T(-0.5) * F[j];
+                        if (gain >= T(1e-4) * Gs[j]) {
+                            alpha = abase * T(1.0 / (1 << j));
+                            accepted = gain > T(0);
+                            lchg = chj[j];
+                        }
+                    }
+                    if (alpha > T(0)) pending = false;
+                    abase *= T(1.0 / (1 << NA));
+                    if (abase < T(1e-12)) pending = false;
+                }
+            }
+            if (lsmode && run && !fast) {
+                if (accepted && lchg) {
+#pragma unroll
+                    for (int k = 0; k < E; ++k) {
+                        const T lk = lam.at(k);
+                        const T dk = bit<E>(bnd, k) ? T(0) : (w[k] - u[k]);
+                        u[k] = clampv(u[k] + alpha * dk, -lk, lk);
+                    }
+                    uchg = true;
+                } else {
+                    stall = true;
+                    run = false;
+                }
+            }
+        } else if (C.uany(pending)) {
             T alpha = T(1), slope = T(0);
             bool accepted = false, lchg = false;
             for (int trial = 0; trial < 30; ++trial) {
