@@ -96,6 +96,67 @@ __device__ __forceinline__ void seg_step(uint32_t nb, uint32_t fbm, uint32_t b, 
     c = bk ? 0.0 : c;
 }
 
+// Backward segment-mean steps in predicated form (float), see seg_mean_c.
+__device__ __forceinline__ void segm1_step(uint32_t bnd, uint32_t fbm, uint32_t b, float s, float cnt,
+                                           float& v, float& sf, float& so, float& co) {
+    asm("{\n\t.reg .pred pb, pf;\n\t.reg .b32 t1, t2;\n\t.reg .f32 r;\n\t"
+        "and.b32 t1, %4, %6;\n\t"
+        "setp.ne.u32 pb, t1, 0;\n\t"
+        "and.b32 t2, %5, %6;\n\t"
+        "setp.ne.u32 pf, t2, 0;\n\t"
+        "rcp.approx.ftz.f32 r, %8;\n\t"
+        "@pf mov.f32 %1, %7;\n\t"
+        "@pb mul.f32 %0, %7, r;\n\t"
+        "mov.f32 %2, %7;\n\t"
+        "mov.f32 %3, %8;\n\t"
+        "@pb mov.f32 %2, 0f00000000;\n\t"
+        "@pb mov.f32 %3, 0f00000000;\n\t}"
+        : "+f"(v), "+f"(sf), "=f"(so), "=f"(co)
+        : "r"(bnd), "r"(fbm), "r"(b), "f"(s), "f"(cnt));
+}
+__device__ __forceinline__ void segm1_step(uint32_t bnd, uint32_t fbm, uint32_t b, double s, double cnt,
+                                           double& v, double& sf, double& so, double& co) {
+    const bool bk = (bnd & b) != 0u, fk = (fbm & b) != 0u;
+    sf = fk ? s : sf;
+    v = bk ? s * rcp_(cnt) : v;
+    so = bk ? 0.0 : s;
+    co = bk ? 0.0 : cnt;
+}
+__device__ __forceinline__ void segm3_step(uint32_t bnd, uint32_t fm, uint32_t ng, uint32_t zs, uint32_t b, float fv,
+                                           float& v, float& cur, float& sd, float& sn, float& sz) {
+    asm("{\n\t.reg .pred pb, pf, pn, pz;\n\t.reg .b32 t1, t2, t3, t4;\n\t.reg .f32 x, d;\n\t"
+        "and.b32 t1, %5, %9;\n\t"
+        "setp.ne.u32 pb, t1, 0;\n\t"
+        "and.b32 t2, %6, %9;\n\t"
+        "setp.ne.u32 pf, t2, 0;\n\t"
+        "and.b32 t3, %7, %9;\n\t"
+        "setp.ne.u32 pn, t3, 0;\n\t"
+        "and.b32 t4, %8, %9;\n\t"
+        "setp.ne.u32 pz, t4, 0;\n\t"
+        "mov.f32 x, %1;\n\t"
+        "@pb mov.f32 x, %0;\n\t"
+        "@pf mov.f32 x, %10;\n\t"
+        "sub.f32 d, x, %1;\n\t"
+        "add.f32 %2, %2, d;\n\t"
+        "@pn add.f32 %3, %3, d;\n\t"
+        "@pz add.f32 %4, %4, d;\n\t"
+        "mov.f32 %0, x;\n\t"
+        "mov.f32 %1, x;\n\t}"
+        : "+f"(v), "+f"(cur), "+f"(sd), "+f"(sn), "+f"(sz)
+        : "r"(bnd), "r"(fm), "r"(ng), "r"(zs), "r"(b), "f"(fv));
+}
+__device__ __forceinline__ void segm3_step(uint32_t bnd, uint32_t fm, uint32_t ng, uint32_t zs, uint32_t b, double fv,
+                                           double& v, double& cur, double& sd, double& sn, double& sz) {
+    double x = (bnd & b) ? v : cur;
+    x = (fm & b) ? fv : x;
+    const double d = x - cur;
+    sd += d;
+    sn += (ng & b) ? d : 0.0;
+    sz += (zs & b) ? d : 0.0;
+    v = x;
+    cur = x;
+}
+
 // m |= b  iff  ug > 0 and au >= thr, as two compares (the second predicated on the
 // first) and one predicated OR -- the ALU pipe is the forward's binding pipe.
 __device__ __forceinline__ void or_if_outward(uint32_t& m, float ug, float au, float thr, uint32_t b) {
@@ -631,12 +692,7 @@ __device__ __forceinline__ void seg_mean_c(T (&v)[E], uint32_t bnd, uint32_t pos
     for (int k = 0; k < E; ++k) {
         s += v[k];
         cnt += T(1);
-        const bool bk = bit<E>(bnd, k);
-        const bool fk = bit<E>(firstb, k);
-        sf = fk ? s : sf;
-        v[k] = bk ? s * rcp_(cnt) : v[k];
-        s = bk ? T(0) : s;
-        cnt = bk ? T(0) : cnt;
+        segm1_step(bnd, firstb, 1u << k, s, cnt, v[k], sf, s, cnt);
     }
     const int hb = 31 - __clz(bnd);
     const bool fl = bnd != 0u;
@@ -654,16 +710,7 @@ __device__ __forceinline__ void seg_mean_c(T (&v)[E], uint32_t bnd, uint32_t pos
     const uint32_t zs = bnd & ~(pos | neg);          // edges with zero sign
     T sd = T(0), sn = T(0), sz = T(0);
 #pragma unroll
-    for (int k = E - 1; k >= 0; --k) {
-        T x = bit<E>(bnd, k) ? v[k] : cur;
-        x = bit<E>(firstm, k) ? fv : x;
-        const T d = x - cur;
-        sd += d;
-        sn += bit<E>(neg, k) ? d : T(0);
-        if (zs) sz += bit<E>(zs, k) ? d : T(0);
-        v[k] = x;
-        cur = x;
-    }
+    for (int k = E - 1; k >= 0; --k) segm3_step(bnd, firstm, neg, zs, 1u << k, fv, v[k], cur, sd, sn, sz);
     const T lp = sd - T(2) * sn - sz;
     lam_part += lp;
 }
