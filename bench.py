@@ -357,6 +357,19 @@ def cpu_baseline(seconds=12.0, rows_per_batch=2048):
                       % (done, el, cores)}
 
 
+def issue_roofline(warp_instr, ms, peaks):
+    """Instruction-issue roofline of the forward op: the executed warp instructions of one
+    launch (ncu, committed profile) over its live duration, against the SM issue peak
+    (148 SMs x 4 schedulers x 1 warp-instruction / clock at the max SM clock)."""
+    if not warp_instr or not ms:
+        return None
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0)) if peaks else 1965.0
+    peak = 148 * 4 * sm_mhz * 1e6
+    ach = warp_instr / (ms * 1e-3)
+    return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-instr/s", "frac": ach / peak,
+            "warp_instr_per_launch": warp_instr, "source": "ncu smsp__inst_executed (profiles/ncu_traffic.json)"}
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_setup(args)
@@ -383,6 +396,8 @@ def run_ours(args):
         "share_of_step": (r["fwd_ms"] if dom == "fwd" else r["bwd_ms"]) / ms_step,
         # the forward is issue-bound: pipe utilisation from the ncu capture
         "pipes_ncu": traffic.get("c2_fwd_pipes" if dom == "fwd" else "c2_bwd_pipes"),
+        "issue": issue_roofline(traffic.get("c2_fwd_warp_instr_per_launch"), r["fwd_ms"], peaks) if dom == "fwd"
+        else None,
         "other_kernel": {"name": "bwd" if dom == "fwd" else "fwd",
                          "achieved": bwd_gbs if dom == "fwd" else fwd_gbs,
                          "frac": (bwd_gbs if dom == "fwd" else fwd_gbs) / peak,

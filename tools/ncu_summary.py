@@ -19,7 +19,7 @@ KEYS = [
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
-    ("sm__inst_executed.sum", "warp instr executed"),
+    ("smsp__inst_executed.sum", "warp instr executed"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__grid_size", "grid"),
@@ -74,12 +74,15 @@ def main():
              "Durations are ncu's; bench.py's live CUDA-event timings are the reported numbers.", ""]
     traffic = {}
     pipe_info = {}
+    warp_instr = {}
     for raw in sorted(glob.glob(os.path.join(src, "%s_*.raw.csv" % tag))):
         name = os.path.basename(raw).replace(".raw.csv", "")
         d = read_raw(raw)
         if not d:
             continue
         s = summarize(d, name)
+        if "warp instr executed" in s and s["warp instr executed"][0]:
+            warp_instr[name] = s["warp instr executed"][0]
         pipe_info[name] = {lab: s[lab][0] for lab in ("issue active %", "ALU pipe % peak", "FMA pipe % peak",
                                                         "achieved occupancy %") if lab in s}
         lines.append("## %s" % name)
@@ -118,6 +121,10 @@ def main():
             tj["c2_fwd_pipes"] = pipes
         elif name.endswith("c2_row_bwd"):
             tj["c2_bwd_pipes"] = pipes
+    # executed warp instructions per launch of the C2 forward op (coarse pre-pass + fine PN)
+    wi = {n: v for n, v in warp_instr.items() if n.endswith(("c2_row_fwd", "c2_coarse"))}
+    if wi:
+        tj["c2_fwd_warp_instr_per_launch"] = sum(wi.values())
     for k, v in traffic.items():
         if k.endswith("c2_row_fwd"):
             tj["c2_fwd_bytes_per_launch"] = v
