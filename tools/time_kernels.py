@@ -65,6 +65,26 @@ def sweep():
             n, rows, f, itn.mean(), itn.max(), f * 1e6 / (rows * n * itn.mean()), rows * n / f / 1e6), flush=True)
 
 
+def long_rows():
+    """f4: long 1D signals (unit step + N(0, 0.1^2) / N(0, 0.5^2) like C2, lambda scaled with n)."""
+    rng = np.random.default_rng(0)
+    for n in (2048, 4096, 8192):
+        rows = (1 << 26) // n
+        y = np.zeros((rows, n), np.float32)
+        y[:, n // 2:] = 1.0
+        y += (rng.standard_normal((rows, n)) * np.where(np.arange(rows) % 2 == 0, 0.1, 0.5)[:, None]).astype(np.float32)
+        yt = torch.as_tensor(y, device="cuda")
+        lam = torch.as_tensor(rng.uniform(0.13, 1.3, rows).astype(np.float32) * np.float32(np.sqrt(n / 1024)),
+                              device="cuda")
+        x, mask, it = tvprox.tv1d_fwd(yt, lam, want_iters=True)
+        itn = (it.cpu().numpy() & 0xffff)
+        f = timeit(lambda: tvprox.tv1d_fwd(yt, lam), reps=5)
+        g = torch.randn_like(yt)
+        bw = timeit(lambda: tvprox.tv1d_bwd(g, mask, _lib.LAM_PER_ROW), reps=5)
+        print("long n %5d rows %6d fwd %.3f ms bwd %.3f ms -> %.1f M rows/s fwd+bwd, %.2f Gsample/s; iters mean %.2f max %d" % (
+            n, rows, f, bw, rows / (f + bw) / 1e3, rows * n / (f + bw) / 1e6, itn.mean(), itn.max()), flush=True)
+
+
 def twod(name):
     w = getattr(workloads, name)()
     X = torch.as_tensor(w.X, device="cuda")
@@ -85,6 +105,8 @@ if __name__ == "__main__":
         sweep()
     if which in ("c2", "all"):
         c2()
+    if which in ("long",):
+        long_rows()
     for n in ("c3", "c4", "c5"):
         if which in (n, "all"):
             twod(n)
