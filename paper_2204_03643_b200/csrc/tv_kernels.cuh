@@ -141,6 +141,9 @@ __device__ __forceinline__ void smem_to_regs(const T* buf, int l, T (&y)[E]) {
     for (int k = 0; k < E; ++k) y[k] = buf[spad(l * E + k)];
 }
 
+#ifndef TVP_COARSE_MAXWPL
+#define TVP_COARSE_MAXWPL 16
+#endif
 // Solve one line held by this lane group: centring, pinning, non-finite
 // detection, PN solve.  Writes the uncentred output into `w` and returns the
 // status (row_iters code).
@@ -191,7 +194,8 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
     for (int k = 0; k < E; ++k) y[k] -= mean;
     // cold solve: initial bound set from the block-restricted problem (coarse_init);
     // lines held by a full warp or more (short lines converge in 3-5 iterations cold)
-    if (!PE && LPR * WPL >= 32 && WPL <= 2 && coarse && n / E >= 3) {
+    if (!PE && LPR * WPL >= 32 && WPL <= TVP_COARSE_MAXWPL && (sizeof(T) == 4 || WPL <= 2) && coarse &&
+        n / E >= 3) {
         uint32_t cp, cn;
         coarse_init<T, E, LPR, WPL>(y, lam.r, n, active, C, xb, cp, cn);
         warm_pos |= cp;

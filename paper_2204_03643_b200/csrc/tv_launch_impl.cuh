@@ -150,9 +150,8 @@ cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStr
     const int split = row_fwd_split();
     if (a.n > 1024) {
         // long 1D rows (f4): one CTA of WPL warps holds the row in registers, E = 16
-        // (fp32) / 8 (fp64) samples per lane; cold start (the coarse solve is for
-        // <= 2 warps per line)
-        a.coarse = 0;
+        // (fp32) / 8 (fp64) samples per lane; in-kernel coarse solve if TVP_COARSE_MAXWPL >= WPL
+        if (TVP_COARSE_MAXWPL < 4) a.coarse = 0;
         if constexpr (sizeof(T) == 4) {
             if (a.n <= 2048) return per_edge ? row_fwd_w_t<T, 16, 4, true, false>(a, s) : row_fwd_w_t<T, 16, 4, false, false>(a, s);
             if (a.n <= 4096) return per_edge ? row_fwd_w_t<T, 16, 8, true, false>(a, s) : row_fwd_w_t<T, 16, 8, false, false>(a, s);
