@@ -130,10 +130,25 @@ struct Comm {
             __syncthreads();
             T ca = T(0);
             int cc = 0;
-            for (int i = 0; i < w; ++i) {
-                const T ra = V(S, 0, i);
-                const int rcf = I(S, i);
-                if (rcf >> 30) { ca = ra; cc = rcf & 0x3fffffff; } else { ca += ra; cc += rcf & 0x3fffffff; }
+            if constexpr (WPL > 2) {
+                // log-depth segmented scan of the WPL warp aggregates on lanes 0..WPL-1
+                T xa = (l < WPL) ? V(S, 0, l) : T(0);
+                int xc = (l < WPL) ? I(S, l) : 0;
+#pragma unroll
+                for (int d = 1; d < WPL; d <<= 1) {
+                    const T a2 = shup<32>(xa, d);
+                    const int c2 = shup<32>(xc, d);
+                    if (l >= d && !(xc >> 30)) { xa += a2; xc = (xc & 0x3fffffff) + (c2 & 0x3fffffff) | (c2 & (1 << 30)); }
+                }
+                ca = __shfl_sync(FULL, xa, w > 0 ? w - 1 : 0);
+                cc = __shfl_sync(FULL, xc, w > 0 ? w - 1 : 0) & 0x3fffffff;
+                if (w == 0) { ca = T(0); cc = 0; }
+            } else {
+                for (int i = 0; i < w; ++i) {
+                    const T ra = V(S, 0, i);
+                    const int rcf = I(S, i);
+                    if (rcf >> 30) { ca = ra; cc = rcf & 0x3fffffff; } else { ca += ra; cc += rcf & 0x3fffffff; }
+                }
             }
             if (!(ecf >> 30)) { ea += ca; ecf += cc; }
         }
@@ -156,8 +171,22 @@ struct Comm {
             if (l == LPR - 1) { V(S, 0, w) = a; V(S, 1, w) = b; I(S, w) = (int)f; }
             __syncthreads();
             T ca = T(0), cb = T(0);
-            for (int i = 0; i < w; ++i) {
-                if (I(S, i)) { ca = V(S, 0, i); cb = V(S, 1, i); } else { ca += V(S, 0, i); cb += V(S, 1, i); }
+            if constexpr (WPL > 2) {
+                T xa = (l < WPL) ? V(S, 0, l) : T(0), xb = (l < WPL) ? V(S, 1, l) : T(0);
+                int xf = (l < WPL) ? I(S, l) : 0;
+#pragma unroll
+                for (int d = 1; d < WPL; d <<= 1) {
+                    const T a2 = shup<32>(xa, d), b2 = shup<32>(xb, d);
+                    const int f2 = shup<32>(xf, d);
+                    if (l >= d && !xf) { xa += a2; xb += b2; xf = f2; }
+                }
+                ca = __shfl_sync(FULL, xa, w > 0 ? w - 1 : 0);
+                cb = __shfl_sync(FULL, xb, w > 0 ? w - 1 : 0);
+                if (w == 0) { ca = T(0); cb = T(0); }
+            } else {
+                for (int i = 0; i < w; ++i) {
+                    if (I(S, i)) { ca = V(S, 0, i); cb = V(S, 1, i); } else { ca += V(S, 0, i); cb += V(S, 1, i); }
+                }
             }
             if (!ef) { ea += ca; eb += cb; }
         }
@@ -203,7 +232,20 @@ struct Comm {
         if (WPL > 1) {
             if (l == 0) { V(S, 0, w) = v; I(S, w) = (int)f; }
             __syncthreads();
-            if (!ef) {
+            if constexpr (WPL > 2) {
+                // nearest flagged warp strictly to the right: log-depth on lanes 0..WPL-1
+                T xv = (l < WPL) ? V(S, 0, l) : T(0);
+                int xf = (l < WPL) ? I(S, l) : 0;
+                if (!xf) xv = T(0);
+#pragma unroll
+                for (int d = 1; d < WPL; d <<= 1) {
+                    const T v2 = shdn<32>(xv, d);
+                    const int f2 = shdn<32>(xf, d);
+                    if (l + d < WPL && !xf) { xv = v2; xf = f2; }
+                }
+                const T r = __shfl_sync(FULL, xv, w + 1 < WPL ? w + 1 : 0);
+                if (!ef && w + 1 < WPL) e = r;
+            } else if (!ef) {
                 for (int i = w + 1; i < WPL; ++i) {
                     if (I(S, i)) { e = V(S, 0, i); break; }
                 }
