@@ -113,20 +113,61 @@ struct Comm {
         return v;
     }
 
-    // Segmented exclusive scan of (a, c) with flag f: combine(L, R) = R.f ? R : (L.a + R.a, L.c + R.c).
-    template <int S>
-    __device__ __forceinline__ void scan_fwd(T& a, int& c, bool f) const {
+    // ---- Segmented scans.  The flags of one solver step are the same for all its
+    // scans (f = "the lane holds a bound edge"), so the lane geometry of the segments
+    // is derived once from a ballot (seg_plan) and each scan then only moves data:
+    //   h  = highest flagged lane <= this lane in the group (the segment head), D = l - h;
+    //   a Hillis-Steele level d adds the partial of lane l - d iff d <= D, which is
+    //   exactly when the flag-carrying form (combine(L, R) = R.f ? R : L + R) adds it,
+    //   so the sums are bitwise those of that form, with one shuffle per level;
+    //   rs = lowest flagged lane strictly above this lane (reverse broadcast source).
+    struct Seg {
+        int D;          // adds allowed for levels d <= D
+        int h;          // segment head lane (absolute), valid if hh
+        bool hh;        // a flagged lane at or below this lane (in the group)
+        bool hx;        // a flagged lane strictly below this lane
+        int rs;         // lowest flagged lane strictly above (absolute), valid if rf
+        bool rf;
+        uint32_t fm;    // ballot of the flags (whole warp)
+    };
+    __device__ __forceinline__ Seg seg_plan(bool f) const {
+        Seg g;
+        const uint32_t lane = threadIdx.x & 31u;
+        const uint32_t gb = lane & ~uint32_t(LPR - 1);
+        const uint32_t fm = __ballot_sync(FULL, f);
+        const uint32_t glo = ~((1u << gb) - 1u);                                     // lanes >= gb
+        const uint32_t ghi = (LPR == 32 || gb + LPR == 32) ? 0xffffffffu : ((1u << (gb + LPR)) - 1u);
+        const uint32_t le = fm & glo & ((2u << lane) - 1u);                          // flagged, <= lane
+        const uint32_t gt = fm & ghi & ~((2u << lane) - 1u);                         // flagged, > lane
+        g.hh = le != 0u;
+        g.h = g.hh ? 31 - __clz(le) : (int)gb;
+        g.D = (int)lane - g.h;
+        g.hx = (le & ~(1u << lane)) != 0u;
+        g.rf = gt != 0u;
+        g.rs = g.rf ? __ffs(gt) - 1 : (int)lane;
+        g.fm = fm;
+        return g;
+    }
+
+    // Segmented exclusive scan of (a, c): a summed; c a sample count with c == E on
+    // lanes without a flag (so its scan is position arithmetic: E per lane since the
+    // head plus the head's own count).
+    template <int S, int E>
+    __device__ __forceinline__ void scan_fwd(const Seg& g, T& a, int& c) const {
+        const uint32_t lane = threadIdx.x & 31u;
 #pragma unroll
         for (int d = 1; d < LPR; d <<= 1) {
-            T a2 = shup<LPR>(a, d);
-            int cf2 = shup<LPR>(c | (f ? (1 << 30) : 0), d);
-            if (l >= d && !f) { a += a2; c += cf2 & 0x3fffffff; f = (cf2 >> 30) & 1; }
+            const T a2 = shup<LPR>(a, d);
+            if (d <= g.D) a += a2;
         }
+        const int ch = __shfl_sync(FULL, c, g.h);
+        const int ci = g.hh ? g.D * E + ch : (g.D + 1) * E;                  // inclusive count
         T ea = shup<LPR>(a, 1);
-        int ecf = shup<LPR>(c | (f ? (1 << 30) : 0), 1);
+        int ecf = shup<LPR>(ci | (g.hh ? (1 << 30) : 0), 1);
         if (l == 0) { ea = T(0); ecf = 0; }
+        (void)lane;
         if (WPL > 1) {
-            if (l == LPR - 1) { V(S, 0, w) = a; I(S, w) = c | (f ? (1 << 30) : 0); }
+            if (l == LPR - 1) { V(S, 0, w) = a; I(S, w) = ci | (g.hh ? (1 << 30) : 0); }
             __syncthreads();
             T ca = T(0);
             int cc = 0;
@@ -157,18 +198,16 @@ struct Comm {
     }
     // Segmented exclusive scan of two summed values (a, b).
     template <int S>
-    __device__ __forceinline__ void scan_fwd2(T& a, T& b, bool f) const {
+    __device__ __forceinline__ void scan_fwd2(const Seg& g, T& a, T& b) const {
 #pragma unroll
         for (int d = 1; d < LPR; d <<= 1) {
-            T a2 = shup<LPR>(a, d), b2 = shup<LPR>(b, d);
-            int f2 = shup<LPR>((int)f, d);
-            if (l >= d && !f) { a += a2; b += b2; f = f2 != 0; }
+            const T a2 = shup<LPR>(a, d), b2 = shup<LPR>(b, d);
+            if (d <= g.D) { a += a2; b += b2; }
         }
         T ea = shup<LPR>(a, 1), eb = shup<LPR>(b, 1);
-        int ef = shup<LPR>((int)f, 1);
-        if (l == 0) { ea = T(0); eb = T(0); ef = 0; }
+        if (l == 0) { ea = T(0); eb = T(0); }
         if (WPL > 1) {
-            if (l == LPR - 1) { V(S, 0, w) = a; V(S, 1, w) = b; I(S, w) = (int)f; }
+            if (l == LPR - 1) { V(S, 0, w) = a; V(S, 1, w) = b; I(S, w) = (int)g.hh; }
             __syncthreads();
             T ca = T(0), cb = T(0);
             if constexpr (WPL > 2) {
@@ -188,49 +227,21 @@ struct Comm {
                     if (I(S, i)) { ca = V(S, 0, i); cb = V(S, 1, i); } else { ca += V(S, 0, i); cb += V(S, 1, i); }
                 }
             }
-            if (!ef) { ea += ca; eb += cb; }
+            if (!g.hx) { ea += ca; eb += cb; }
         }
         a = ea;
         b = eb;
     }
-    // Value of the nearest flagged line lane strictly to the left (0 if none).
+    // Value of the nearest flagged line lane strictly to the right (0 if none): one
+    // shuffle from the plan's source lane.
     template <int S>
-    __device__ __forceinline__ int scan_last(int v, bool f) const {
-#pragma unroll
-        for (int d = 1; d < LPR; d <<= 1) {
-            int v2 = shup<LPR>(v, d);
-            int f2 = shup<LPR>((int)f, d);
-            if (l >= d && !f) { v = v2; f = f2 != 0; }
-        }
-        int e = shup<LPR>(v, 1);
-        int ef = shup<LPR>((int)f, 1);
-        if (l == 0) { e = 0; ef = 0; }
+    __device__ __forceinline__ T scan_rev(const Seg& g, T v) const {
+        T e = __shfl_sync(FULL, v, g.rs);
+        if (!g.rf) e = T(0);
         if (WPL > 1) {
-            if (l == LPR - 1) { I(S, w) = f ? ((v + 2) | (1 << 30)) : 0; }   // small ints only
-            __syncthreads();
-            if (!ef) {
-                for (int i = w - 1; i >= 0; --i) {
-                    const int q = I(S, i);
-                    if (q >> 30) { e = (q & 0xffff) - 2; break; }
-                }
-            }
-        }
-        return e;
-    }
-    // Value of the nearest flagged line lane strictly to the right (0 if none).
-    template <int S>
-    __device__ __forceinline__ T scan_rev(T v, bool f) const {
-#pragma unroll
-        for (int d = 1; d < LPR; d <<= 1) {
-            T v2 = shdn<LPR>(v, d);
-            int f2 = shdn<LPR>((int)f, d);
-            if (l + d < LPR && !f) { v = v2; f = f2 != 0; }
-        }
-        T e = shdn<LPR>(v, 1);
-        int ef = shdn<LPR>((int)f, 1);
-        if (l + 1 >= LPR) { e = T(0); ef = 0; }
-        if (WPL > 1) {
-            if (l == 0) { V(S, 0, w) = v; I(S, w) = (int)f; }
+            // the warp's inclusive-from-the-left value: its lowest flagged lane's v
+            const T vf = __shfl_sync(FULL, v, g.fm ? __ffs(g.fm) - 1 : 0);
+            if (l == 0) { V(S, 0, w) = vf; I(S, w) = g.fm != 0u; }
             __syncthreads();
             if constexpr (WPL > 2) {
                 // nearest flagged warp strictly to the right: log-depth on lanes 0..WPL-1
@@ -244,8 +255,8 @@ struct Comm {
                     if (l + d < WPL && !xf) { xv = v2; xf = f2; }
                 }
                 const T r = __shfl_sync(FULL, xv, w + 1 < WPL ? w + 1 : 0);
-                if (!ef && w + 1 < WPL) e = r;
-            } else if (!ef) {
+                if (!g.rf && w + 1 < WPL) e = r;
+            } else if (!g.rf) {
                 for (int i = w + 1; i < WPL; ++i) {
                     if (I(S, i)) { e = V(S, 0, i); break; }
                 }

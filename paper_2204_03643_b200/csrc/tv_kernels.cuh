@@ -144,6 +144,10 @@ __device__ __forceinline__ void smem_to_regs(const T* buf, int l, T (&y)[E]) {
 #ifndef TVP_COARSE_MAXWPL
 #define TVP_COARSE_MAXWPL 16
 #endif
+// Lines held by fewer lanes than this never take the coarse initial bound set.
+#ifndef TVP_COARSE_MINLANES
+#define TVP_COARSE_MINLANES 16
+#endif
 // Solve one line held by this lane group: centring, pinning, non-finite
 // detection, PN solve.  Writes the uncentred output into `w` and returns the
 // status (row_iters code).
@@ -194,7 +198,7 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
     for (int k = 0; k < E; ++k) y[k] -= mean;
     // cold solve: initial bound set from the block-restricted problem (coarse_init);
     // lines held by a full warp or more (short lines converge in 3-5 iterations cold)
-    if (!PE && LPR * WPL >= 32 && WPL <= TVP_COARSE_MAXWPL && (sizeof(T) == 4 || WPL <= 2) && coarse &&
+    if (!PE && LPR * WPL >= TVP_COARSE_MINLANES && WPL <= TVP_COARSE_MAXWPL && (sizeof(T) == 4 || WPL <= 2) && coarse &&
         n / E >= 3) {
         uint32_t cp, cn;
         coarse_init<T, E, LPR, WPL>(y, lam.r, n, active, C, xb, cp, cn);
@@ -216,11 +220,17 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
 // same-box A/B: the issue-bound PN loops gain from occupancy until they would spill;
 // fp64 and the long-register-line geometries keep their natural allocation).
 // TVP_ROW_MINB / TVP_ROWW_MINB / TVP_COL_MINB override them for A/B builds.
+#ifndef TVP_ROW14_MINB
+#define TVP_ROW14_MINB 4
+#endif
+#ifndef TVP_COL14_MINB
+#define TVP_COL14_MINB 2
+#endif
 template <typename T, int E> constexpr int row_minb() {
 #ifdef TVP_ROW_MINB
     return TVP_ROW_MINB;
 #else
-    return sizeof(T) == 4 ? (E <= 8 ? 6 : 1) : 1;
+    return sizeof(T) == 4 ? (E <= 8 ? 6 : (E == 14 ? TVP_ROW14_MINB : 1)) : 1;
 #endif
 }
 template <typename T, int E, int WPL> constexpr int roww_minb() {
@@ -234,7 +244,7 @@ template <typename T, int E> constexpr int col_minb() {
 #ifdef TVP_COL_MINB
     return TVP_COL_MINB;
 #else
-    return (sizeof(T) == 4 && E <= 8) ? 2 : 1;
+    return (sizeof(T) == 4 && E <= 8) ? 2 : ((sizeof(T) == 4 && E == 14) ? TVP_COL14_MINB : 1);
 #endif
 }
 
@@ -316,7 +326,7 @@ k_row_fwd(RowFwdArgs<T> a) {
         // partial words it touches are OR-ed into a warp-private word buffer with
         // shared-memory atomics (n <= 512 here, so a line has <= 32 words)
         if (a.mask_out) {
-            if (l < 8 || LPR == 32) mwb[grp * (32 / G) + l] = 0u;
+            mwb[grp * (32 / G) + l] = 0u;                  // LPR == 32 / G word slots per line
             const T wnx = shdn<LPR>(w[0], 1);
             const int e0 = l * E;
             const int wlo = e0 >> 4;

@@ -40,8 +40,12 @@ static int persistent_grid(K kern, int threads, size_t smem, int64_t work_blocks
 
 #define TVP_GEO_DISPATCH(n, ...)                                               \
     do {                                                                       \
-        Geo g_ = pick_geo(n);                                                  \
-        if (g_.LPR == 8) {                                                     \
+        Geo g_ = pick_geo(n, (int)sizeof(T));                                  \
+        if (g_.LPR == 16) {                                                    \
+            if constexpr (sizeof(T) == 4) {                                    \
+                constexpr int E_ = 14, L_ = 16; __VA_ARGS__;                   \
+            }                                                                  \
+        } else if (g_.LPR == 8) {                                              \
             switch (g_.E) {                                                    \
                 case 2: { constexpr int E_ = 2, L_ = 8; __VA_ARGS__; } break;         \
                 case 4: { constexpr int E_ = 4, L_ = 8; __VA_ARGS__; } break;         \
@@ -77,9 +81,20 @@ static int row_fwd_split() {
 #endif
 constexpr int kColWPB = TVP_COL_WPB;
 
+// TVP_COARSE16=0 (A/B): half-warp lines (LPR = 16) solve cold without the coarse start.
+static bool coarse16_knob() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TVP_COARSE16");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
 template <typename T, int E, int LPR, bool PE, bool DYK>
-static cudaError_t row_fwd_t(const RowFwdArgs<T>& a, cudaStream_t s) {
+static cudaError_t row_fwd_t(RowFwdArgs<T> a, cudaStream_t s) {
     constexpr int G = 32 / LPR;
+    if (LPR < 32 && !coarse16_knob()) a.coarse = 0;
     constexpr int LP = line_pitch<E, LPR>();
     const size_t smem = (size_t)kRowWPB * (DYK ? 2 : 1) * G * LP * sizeof(T) + (size_t)kRowWPB * 32 * 4;
     auto kern = k_row_fwd<T, E, LPR, PE, DYK, kRowWPB>;
@@ -210,6 +225,7 @@ static cudaError_t col_fwd_t(ColFwdArgs<T> a, cudaStream_t s) {
     constexpr int LP = line_pitch<E, LPR>();
     constexpr int TC = col_tile<LPR>();
     a.TC = TC;
+    if (LPR < 32 && !coarse16_knob()) a.coarse = 0;
     const size_t smem = (size_t)2 * TC * LP * sizeof(T) + (size_t)kColWPB * 64 * 4;
     auto kern = k_col_fwd<T, E, LPR, kColWPB>;
     const int64_t tiles = a.planes * ((a.W + TC - 1) / TC);

@@ -31,8 +31,6 @@
 
 namespace tvp {
 
-template <int W> struct Log2 { static constexpr int v = 1 + Log2<W / 2>::v; };
-template <> struct Log2<1> { static constexpr int v = 0; };
 
 // Per-lane view of lambda: one value per line, or one per edge held in registers.
 template <typename T, int E, bool PE>
@@ -61,6 +59,13 @@ __device__ __forceinline__ void padd2(uint32_t m, uint32_t b, double& a0, double
 // Largest E for which the segment pass uses the predicated-move form below (same-box
 // A/B: it wins for the short 2D lines, E = 7, and loses for E = 16 and the coarse
 // E = 2 lines, where the compiler's own select scheduling is better).
+// Predicated-move forms of the P3 broadcast and the P4 running-sum restarts (A/B knobs).
+#ifndef TVP_P3_PTX
+#define TVP_P3_PTX 0
+#endif
+#ifndef TVP_P4_PTX
+#define TVP_P4_PTX 0
+#endif
 #ifndef TVP_SEG_PTX_MAXE
 #define TVP_SEG_PTX_MAXE 8
 #endif
@@ -157,6 +162,42 @@ __device__ __forceinline__ void segm3_step(uint32_t bnd, uint32_t fm, uint32_t n
     cur = x;
 }
 
+// P3 reverse-broadcast step with predicated moves (the ALU pipe binds the forward;
+// a predicated move issues on the FMA pipe, a select on the ALU pipe): off the bound
+// edges the sample takes the running segment value, up to the lane's first bound it
+// takes the carried first-segment value.
+__device__ __forceinline__ void p3_step(uint32_t bnd, uint32_t firstm, uint32_t b, float fv, float& wk, float cur) {
+    asm("{\n\t.reg .pred p, q;\n\t.reg .b32 t1, t2;\n\t"
+        "and.b32 t1, %1, %3;\n\t"
+        "setp.eq.u32 p, t1, 0;\n\t"
+        "and.b32 t2, %2, %3;\n\t"
+        "setp.ne.u32 q, t2, 0;\n\t"
+        "@p mov.f32 %0, %5;\n\t"
+        "@q mov.f32 %0, %4;\n\t}"
+        : "+f"(wk) : "r"(bnd), "r"(firstm), "r"(b), "f"(fv), "f"(cur));
+}
+__device__ __forceinline__ void p3_step(uint32_t bnd, uint32_t firstm, uint32_t b, double fv, double& wk, double cur) {
+    double v = (bnd & b) ? wk : cur;
+    wk = (firstm & b) ? fv : v;
+}
+// P4 running sums restarted at bound edges: r = u_k, A = |u_k| there (predicated moves).
+__device__ __forceinline__ void p4_restart(uint32_t bnd, uint32_t b, float uk, float t, float& r, float& A) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t1;\n\t.reg .f32 at;\n\t"
+        "and.b32 t1, %2, %3;\n\t"
+        "setp.ne.u32 p, t1, 0;\n\t"
+        "add.f32 %0, %0, %5;\n\t"
+        "abs.f32 at, %5;\n\t"
+        "add.f32 %1, %1, at;\n\t"
+        "@p mov.f32 %0, %4;\n\t"
+        "@p abs.f32 %1, %4;\n\t}"
+        : "+f"(r), "+f"(A) : "r"(bnd), "r"(b), "f"(uk), "f"(t));
+}
+__device__ __forceinline__ void p4_restart(uint32_t bnd, uint32_t b, double uk, double t, double& r, double& A) {
+    const bool bk = (bnd & b) != 0u;
+    r = bk ? uk : r + t;
+    A = bk ? fabs(uk) : A + fabs(t);
+}
+
 // m |= b  iff  ug > 0 and au >= thr, as two compares (the second predicated on the
 // first) and one predicated OR -- the ALU pipe is the forward's binding pipe.
 __device__ __forceinline__ void or_if_outward(uint32_t& m, float ug, float au, float thr, uint32_t b) {
@@ -178,56 +219,6 @@ __device__ __forceinline__ void or_if_outward(uint32_t& m, double ug, double au,
 __device__ __forceinline__ int prev_bit(uint32_t m, int k) {
     uint32_t mm = k >= 32 ? m : (m & ((1u << k) - 1u));
     return 31 - __clz(mm);
-}
-
-// ---------------------------------------------------------------------------
-// Segmented exclusive scans over the LPR lanes of a line group.
-// fwd: carry of (a, c, f) with combine(L, R) = R.f ? R : (L.a + R.a, L.c + R.c, L.f);
-//      identity (0, 0, false).  c < 2^30.
-// ---------------------------------------------------------------------------
-template <int LPR, typename T>
-__device__ __forceinline__ void seg_scan_fwd(T& a, int& c, bool f, int l) {
-#pragma unroll
-    for (int d = 1; d < LPR; d <<= 1) {
-        T a2 = shup<LPR>(a, d);
-        int cf2 = shup<LPR>(c | (f ? (1 << 30) : 0), d);
-        if (l >= d && !f) {
-            a += a2;
-            c += cf2 & 0x3fffffff;
-            f = (cf2 >> 30) & 1;
-        }
-    }
-    T ea = shup<LPR>(a, 1);
-    int ec = shup<LPR>(c, 1);
-    a = (l == 0) ? T(0) : ea;
-    c = (l == 0) ? 0 : (ec & 0x3fffffff);
-}
-
-// fwd with two summed values (a, b) and a flag.
-template <int LPR, typename T>
-__device__ __forceinline__ void seg_scan_fwd2(T& a, T& b, bool f, int l) {
-#pragma unroll
-    for (int d = 1; d < LPR; d <<= 1) {
-        T a2 = shup<LPR>(a, d), b2 = shup<LPR>(b, d);
-        int f2 = shup<LPR>((int)f, d);
-        if (l >= d && !f) { a += a2; b += b2; f = f2 != 0; }
-    }
-    T ea = shup<LPR>(a, 1), eb = shup<LPR>(b, 1);
-    a = (l == 0) ? T(0) : ea;
-    b = (l == 0) ? T(0) : eb;
-}
-
-// rev: value of the nearest flagged lane strictly to the right (0 if none).
-template <int LPR, typename T>
-__device__ __forceinline__ T seg_scan_rev(T v, bool f, int l) {
-#pragma unroll
-    for (int d = 1; d < LPR; d <<= 1) {
-        T v2 = shdn<LPR>(v, d);
-        int f2 = shdn<LPR>((int)f, d);
-        if (l + d < LPR && !f) { v = v2; f = f2 != 0; }
-    }
-    T e = shdn<LPR>(v, 1);
-    return (l + 1 < LPR) ? e : T(0);
 }
 
 // Iterations after which a line switches from projected full Newton steps to the
@@ -334,23 +325,29 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         const int cnt_tail = E - 1 - hb;
         T cs = s;
         int cc = cnt_tail;
-        C.template scan_fwd<2>(cs, cc, fl);
+        const auto sg = C.seg_plan(fl);               // segment geometry of this step's scans
+        C.template scan_fwd<2, E>(sg, cs, cc);
 
         // ---------------- P2/P3: the lane's first segment gets the carry; reverse
         // broadcast of each segment's value to its samples.
         const int fb = __ffs(bnd) - 1;                // -1 if none
         const uint32_t firstm = bnd ? ((bnd & (0u - bnd)) * 2u - 1u) : 0u;   // bits 0..fb
         const T fv = (numf + cs) * rcp_(T(fb + 1 + cc));
-        T cur = C.template scan_rev<3>(fv, fl);
+        T cur = C.template scan_rev<3>(sg, fv);
         // (the same reverse pass sums xhat - y over the lane's open tail: the lane
         // aggregate of the uhat scan below, accumulated term by term)
         const uint32_t tailm = fl ? ~((2u << hb) - 1u) : 0xffffffffu;
         T rt = T(0), at = T(0);
 #pragma unroll
         for (int k = E - 1; k >= 0; --k) {
+#if TVP_P3_PTX
+            p3_step(bnd, firstm, 1u << k, fv, w[k], cur);
+            const T v = w[k];
+#else
             T v = bit<E>(bnd, k) ? w[k] : cur;
             v = bit<E>(firstm, k) ? fv : v;
             w[k] = v;
+#endif
             cur = v;
             const T t = v - y[k];
             padd2(tailm, 1u << k, rt, t, at, fabs(t));
@@ -365,7 +362,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         // same pass and keeps xhat in w; LS mode writes uhat to w for the search.
         T r = ub + rt;
         T A = fabs(ub) + at;
-        C.template scan_fwd2<4>(r, A, fl);
+        C.template scan_fwd2<4>(sg, r, A);
         const T xnext = C.template next<5>(w[0]);
         const bool lsmode = C.uany(run && !first && (it + 1 >= kLsAfter));
         bool ok = true, clip = false, chg = false;
@@ -386,9 +383,13 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                 const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
                 const T t = xh - y[k];
                 const T lk = lam.at(k);
+#if TVP_P4_PTX
+                p4_restart(bnd, 1u << k, u[k], t, r, A);
+#else
                 const bool bk = bit<E>(bnd, k);
                 r = bk ? u[k] : r + t;
                 A = bk ? fabs(u[k]) : A + fabs(t);
+#endif
                 const T q = u[k] * (xh1 - xh);
                 const T e = fabs(r) - fma(slackA, A, lk * slack1);
                 vio += (fabs(q) - q) + (e + fabs(e));
@@ -698,7 +699,8 @@ __device__ __forceinline__ void seg_mean_c(T (&v)[E], uint32_t bnd, uint32_t pos
     const bool fl = bnd != 0u;
     T cs = s;
     int cc = E - 1 - hb;
-    C.template scan_fwd<0>(cs, cc, fl);
+    const auto sg = C.seg_plan(fl);
+    C.template scan_fwd<0, E>(sg, cs, cc);
     const int fb = __ffs(bnd) - 1;
     const uint32_t firstm = bnd ? (firstb * 2u - 1u) : 0u;
     const T fv = (sf + cs) * rcp_(T(fb + 1 + cc));
@@ -706,7 +708,7 @@ __device__ __forceinline__ void seg_mean_c(T (&v)[E], uint32_t bnd, uint32_t pos
     // gradient in edge form, sum_e s_e (mean_L(e) - mean_R(e)): d = x_k - (value to
     // the right) is exactly 0 inside a segment, so sum_e s_e d_e = sum d - 2 sum_neg d
     // - sum_bnd d, the last term over edges coded "boundary" (s = 0: lam = 0, pinned).
-    T cur = C.template scan_rev<2>(fv, fl);
+    T cur = C.template scan_rev<2>(sg, fv);
     const uint32_t zs = bnd & ~(pos | neg);          // edges with zero sign
     T sd = T(0), sn = T(0), sz = T(0);
 #pragma unroll

@@ -22,6 +22,14 @@ static bool fused2d_default() {
     return !(e && atoi(e) == 0);
 }
 static bool g_fused2d = fused2d_default();
+int geo16_knob() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TVP_GEO16");
+        v = e ? atoi(e) : TVP_GEO16_DEFAULT;
+    }
+    return v;
+}
 }  // namespace tvp
 
 using namespace tvp;
