@@ -185,10 +185,13 @@ struct Comm {
                 cc = __shfl_sync(FULL, xc, w > 0 ? w - 1 : 0) & 0x3fffffff;
                 if (w == 0) { ca = T(0); cc = 0; }
             } else {
-                for (int i = 0; i < w; ++i) {
-                    const T ra = V(S, 0, i);
-                    const int rcf = I(S, i);
-                    if (rcf >> 30) { ca = ra; cc = rcf & 0x3fffffff; } else { ca += ra; cc += rcf & 0x3fffffff; }
+#pragma unroll
+                for (int i = 0; i < WPL - 1; ++i) {
+                    if (i < w) {
+                        const T ra = V(S, 0, i);
+                        const int rcf = I(S, i);
+                        if (rcf >> 30) { ca = ra; cc = rcf & 0x3fffffff; } else { ca += ra; cc += rcf & 0x3fffffff; }
+                    }
                 }
             }
             if (!(ecf >> 30)) { ea += ca; ecf += cc; }
@@ -223,8 +226,11 @@ struct Comm {
                 cb = __shfl_sync(FULL, xb, w > 0 ? w - 1 : 0);
                 if (w == 0) { ca = T(0); cb = T(0); }
             } else {
-                for (int i = 0; i < w; ++i) {
-                    if (I(S, i)) { ca = V(S, 0, i); cb = V(S, 1, i); } else { ca += V(S, 0, i); cb += V(S, 1, i); }
+#pragma unroll
+                for (int i = 0; i < WPL - 1; ++i) {
+                    if (i < w) {
+                        if (I(S, i)) { ca = V(S, 0, i); cb = V(S, 1, i); } else { ca += V(S, 0, i); cb += V(S, 1, i); }
+                    }
                 }
             }
             if (!g.hx) { ea += ca; eb += cb; }
@@ -257,8 +263,10 @@ struct Comm {
                 const T r = __shfl_sync(FULL, xv, w + 1 < WPL ? w + 1 : 0);
                 if (!g.rf && w + 1 < WPL) e = r;
             } else if (!g.rf) {
-                for (int i = w + 1; i < WPL; ++i) {
-                    if (I(S, i)) { e = V(S, 0, i); break; }
+                // nearest flagged warp to the right: the last assignment (lowest i > w) wins
+#pragma unroll
+                for (int i = WPL - 1; i >= 1; --i) {
+                    if (i > w && I(S, i)) e = V(S, 0, i);
                 }
             }
         }

@@ -59,13 +59,24 @@ __device__ __forceinline__ void padd2(uint32_t m, uint32_t b, double& a0, double
 // Largest E for which the segment pass uses the predicated-move form below (same-box
 // A/B: it wins for the short 2D lines, E = 7, and loses for E = 16 and the coarse
 // E = 2 lines, where the compiler's own select scheduling is better).
-// Predicated-move forms of the P3 broadcast and the P4 running-sum restarts (A/B knobs).
-#ifndef TVP_P3_PTX
-#define TVP_P3_PTX 0
+// Predicated-move forms of the P3 broadcast and the P4 running-sum restarts, per
+// register geometry from same-box A/B runs: P4 wins except for
+// the E = 14 half-warp lines (C5), P3 only for one-warp E = 16 lines (C4).
+// TVP_P3_PTX / TVP_P4_PTX = 0 | 1 force them off / on everywhere.
+template <int E, int LPR, int WPL> constexpr bool p3_ptx() {
+#ifdef TVP_P3_PTX
+    return TVP_P3_PTX != 0;
+#else
+    return E == 16 && LPR == 32 && WPL == 1;
 #endif
-#ifndef TVP_P4_PTX
-#define TVP_P4_PTX 0
+}
+template <int E, int LPR, int WPL> constexpr bool p4_ptx() {
+#ifdef TVP_P4_PTX
+    return TVP_P4_PTX != 0;
+#else
+    return E != 14;
 #endif
+}
 #ifndef TVP_SEG_PTX_MAXE
 #define TVP_SEG_PTX_MAXE 8
 #endif
@@ -340,14 +351,15 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         T rt = T(0), at = T(0);
 #pragma unroll
         for (int k = E - 1; k >= 0; --k) {
-#if TVP_P3_PTX
-            p3_step(bnd, firstm, 1u << k, fv, w[k], cur);
-            const T v = w[k];
-#else
-            T v = bit<E>(bnd, k) ? w[k] : cur;
-            v = bit<E>(firstm, k) ? fv : v;
-            w[k] = v;
-#endif
+            T v;
+            if constexpr (p3_ptx<E, LPR, WPL>()) {
+                p3_step(bnd, firstm, 1u << k, fv, w[k], cur);
+                v = w[k];
+            } else {
+                v = bit<E>(bnd, k) ? w[k] : cur;
+                v = bit<E>(firstm, k) ? fv : v;
+                w[k] = v;
+            }
             cur = v;
             const T t = v - y[k];
             padd2(tailm, 1u << k, rt, t, at, fabs(t));
@@ -383,13 +395,13 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                 const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
                 const T t = xh - y[k];
                 const T lk = lam.at(k);
-#if TVP_P4_PTX
-                p4_restart(bnd, 1u << k, u[k], t, r, A);
-#else
-                const bool bk = bit<E>(bnd, k);
-                r = bk ? u[k] : r + t;
-                A = bk ? fabs(u[k]) : A + fabs(t);
-#endif
+                if constexpr (p4_ptx<E, LPR, WPL>()) {
+                    p4_restart(bnd, 1u << k, u[k], t, r, A);
+                } else {
+                    const bool bk = bit<E>(bnd, k);
+                    r = bk ? u[k] : r + t;
+                    A = bk ? fabs(u[k]) : A + fabs(t);
+                }
                 const T q = u[k] * (xh1 - xh);
                 const T e = fabs(r) - fma(slackA, A, lk * slack1);
                 vio += (fabs(q) - q) + (e + fabs(e));
