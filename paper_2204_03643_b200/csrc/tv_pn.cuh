@@ -56,9 +56,6 @@ __device__ __forceinline__ void padd2(uint32_t m, uint32_t b, double& a0, double
     if (m & b) { a0 += x0; a1 += x1; }
 }
 
-// Largest E for which the segment pass uses the predicated-move form below (same-box
-// A/B: it wins for the short 2D lines, E = 7, and loses for E = 16 and the coarse
-// E = 2 lines, where the compiler's own select scheduling is better).
 // Predicated-move forms of the P3 broadcast and the P4 running-sum restarts, per
 // register geometry from same-box A/B runs: P4 wins except for
 // the E = 14 half-warp lines (C5), P3 only for one-warp E = 16 lines (C4).
@@ -77,9 +74,21 @@ template <int E, int LPR, int WPL> constexpr bool p4_ptx() {
     return E != 14;
 #endif
 }
+// Largest E for which the segment pass uses the predicated-move form below (same-box
+// A/B: it wins for the short 2D lines, E = 7, and loses for the two-warp E = 16 and the coarse
+// E = 2 lines, where the compiler's own select scheduling is better).
 #ifndef TVP_SEG_PTX_MAXE
 #define TVP_SEG_PTX_MAXE 8
 #endif
+// ... and beyond it for the E = 14 half-warp lines (C5: fwd -4 %) and one-warp E = 16
+// lines (C4: -2.5 %), same-box A/B (TVP_SEG_PTX_ALL=1 forces it for every E >= 4).
+template <int E, int WPL> constexpr bool seg_ptx() {
+#ifdef TVP_SEG_PTX_ALL
+    return E >= 4;
+#else
+    return E >= 4 && (E <= TVP_SEG_PTX_MAXE || E == 14 || (E == 16 && WPL == 1));
+#endif
+}
 // One sample of the lane-local segment pass (P1b) with predicated moves: on a bound
 // edge (bit b of nb) the segment value num / cnt (num itself on the lane's first bound,
 // which still lacks its carry) is stored and the running sums restart.
@@ -312,7 +321,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             s += y[k];
             cnt += T(1);
             const T num = s + u[k];
-            if (E >= 4 && E <= TVP_SEG_PTX_MAXE) {
+            if constexpr (seg_ptx<E, WPL>()) {
                 seg_step(nb, firstb, 1u << k, num, cnt, u[k], w[k], numf, ub, s, cnt);
             } else {
                 const bool bk = bit<E>(nb, k);
