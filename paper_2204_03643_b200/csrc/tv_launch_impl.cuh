@@ -76,10 +76,24 @@ static int row_fwd_split() {
     }
     return v;
 }
-#ifndef TVP_COL_WPB
-#define TVP_COL_WPB 8
+// Warps per column-tile CTA (tile = WPB x 32 / LPR lines, x2 for one-warp lines), per
+// kernel and geometry from same-box A/B runs: fp32 one-warp
+// E = 16 column solves (C4) 4 warps, E = 14 column adjoints (C5) 4 warps, otherwise 8.
+// TVP_COL_WPB forces one value for every column kernel (A/B builds).
+template <typename T, int E, int LPR> constexpr int col_wpb_fwd() {
+#ifdef TVP_COL_WPB
+    return TVP_COL_WPB;
+#else
+    return (sizeof(T) == 4 && E == 16 && LPR == 32) ? 4 : 8;
 #endif
-constexpr int kColWPB = TVP_COL_WPB;
+}
+template <typename T, int E, int LPR> constexpr int col_wpb_bwd() {
+#ifdef TVP_COL_WPB
+    return TVP_COL_WPB;
+#else
+    return (sizeof(T) == 4 && E == 14) ? 4 : 8;
+#endif
+}
 
 // TVP_COARSE16=0 (A/B): half-warp lines (LPR = 16) solve cold without the coarse start.
 static bool coarse16_knob() {
@@ -218,19 +232,20 @@ no_pass:
     return e;
 }
 
-template <int LPR> constexpr int col_tile() { return kColWPB * (32 / LPR) * (LPR == 32 ? 2 : 1); }
+template <int WPB, int LPR> constexpr int col_tile() { return WPB * (32 / LPR) * (LPR == 32 ? 2 : 1); }
 
 template <typename T, int E, int LPR>
 static cudaError_t col_fwd_t(ColFwdArgs<T> a, cudaStream_t s) {
+    constexpr int WPB = col_wpb_fwd<T, E, LPR>();
     constexpr int LP = line_pitch<E, LPR>();
-    constexpr int TC = col_tile<LPR>();
+    constexpr int TC = col_tile<WPB, LPR>();
     a.TC = TC;
     if (LPR < 32 && !coarse16_knob()) a.coarse = 0;
-    const size_t smem = (size_t)2 * TC * LP * sizeof(T) + (size_t)kColWPB * 64 * 4;
-    auto kern = k_col_fwd<T, E, LPR, kColWPB>;
+    const size_t smem = (size_t)2 * TC * LP * sizeof(T) + (size_t)WPB * 64 * 4;
+    auto kern = k_col_fwd<T, E, LPR, WPB>;
     const int64_t tiles = a.planes * ((a.W + TC - 1) / TC);
-    const int grid = persistent_grid(kern, kColWPB * 32, smem, tiles);
-    kern<<<grid, kColWPB * 32, smem, s>>>(a);
+    const int grid = persistent_grid(kern, WPB * 32, smem, tiles);
+    kern<<<grid, WPB * 32, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }
@@ -311,13 +326,14 @@ cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, 
 template <typename T, int E, int LPR>
 static cudaError_t col_bwd_t(ColBwdArgs<T> a, cudaStream_t s) {
     constexpr int LP = line_pitch<E, LPR>();
-    constexpr int TC = col_tile<LPR>();
+    constexpr int WPB = col_wpb_bwd<T, E, LPR>();
+    constexpr int TC = col_tile<WPB, LPR>();
     a.TC = TC;
     const size_t smem = (size_t)2 * TC * LP * sizeof(T);
-    auto kern = k_col_bwd<T, E, LPR, kColWPB>;
+    auto kern = k_col_bwd<T, E, LPR, WPB>;
     const int64_t tiles = a.planes * ((a.W + TC - 1) / TC);
-    const int grid = persistent_grid(kern, kColWPB * 32, smem, tiles);
-    kern<<<grid, kColWPB * 32, smem, s>>>(a);
+    const int grid = persistent_grid(kern, WPB * 32, smem, tiles);
+    kern<<<grid, WPB * 32, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }
