@@ -326,6 +326,8 @@ def bench_c5(args, ws, rank, local):
     return {
         "metric": "2D TV prox fwd+bwd Mpixel/s (C5: 256x3x224x224, per-channel lambda, K=4, fp32)",
         "value": px_total / (ms * 1e-3) / 1e6, "unit": "Mpixel/s", "ms_per_step": ms,
+        # one pixel = one NCHW element; the spatial rate counts N*H*W (3 channels per pixel)
+        "spatial_mpx_per_s": px_total / 3 / (ms * 1e-3) / 1e6,
         "fwd_ms": statistics.mean(e[0].elapsed_time(e[1]) for e in evs),
         "bwd_ms": statistics.mean(e[1].elapsed_time(e[2]) for e in evs),
         "scaling": "strong", "images_per_rank": per,

@@ -223,6 +223,12 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
 #ifndef TVP_ROW14_MINB
 #define TVP_ROW14_MINB 4
 #endif
+#ifndef TVP_ROW16_MINB
+#define TVP_ROW16_MINB 4
+#endif
+#ifndef TVP_COL16_MINB
+#define TVP_COL16_MINB 4
+#endif
 #ifndef TVP_COL14_MINB
 #define TVP_COL14_MINB 2
 #endif
@@ -230,7 +236,7 @@ template <typename T, int E> constexpr int row_minb() {
 #ifdef TVP_ROW_MINB
     return TVP_ROW_MINB;
 #else
-    return sizeof(T) == 4 ? (E <= 8 ? 6 : (E == 14 ? TVP_ROW14_MINB : 1)) : 1;
+    return sizeof(T) == 4 ? (E <= 8 ? 6 : (E == 14 ? TVP_ROW14_MINB : (E == 16 ? TVP_ROW16_MINB : 1))) : 1;
 #endif
 }
 template <typename T, int E, int WPL> constexpr int roww_minb() {
@@ -244,7 +250,8 @@ template <typename T, int E> constexpr int col_minb() {
 #ifdef TVP_COL_MINB
     return TVP_COL_MINB;
 #else
-    return (sizeof(T) == 4 && E <= 8) ? 2 : ((sizeof(T) == 4 && E == 14) ? TVP_COL14_MINB : 1);
+    return (sizeof(T) == 4 && E <= 8) ? 2 : ((sizeof(T) == 4 && E == 14) ? TVP_COL14_MINB
+                                             : ((sizeof(T) == 4 && E == 16) ? TVP_COL16_MINB : 1));
 #endif
 }
 
@@ -639,7 +646,7 @@ k_col_fwd(ColFwdArgs<T> a) {
     constexpr int LP = line_pitch<E, LPR>();
     extern __shared__ __align__(16) unsigned char smraw_[];
     T* bufA = reinterpret_cast<T*>(smraw_);
-    constexpr int TC = WPB * (32 / LPR) * (LPR == 32 ? 2 : 1);   // == col_tile<LPR>() of the launcher
+    constexpr int TC = WPB * (32 / LPR) * (LPR == 32 ? 2 : 1);   // == col_tile<WPB, LPR>() of the launcher
     T* bufX = bufA + TC * LP;
     uint32_t* mwb = reinterpret_cast<uint32_t*>(bufX + TC * LP) + (threadIdx.x >> 5) * 64;   // mask words
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -938,7 +945,7 @@ k_col_bwd(ColBwdArgs<T> a) {
     constexpr int LP = line_pitch<E, LPR>();
     extern __shared__ __align__(16) unsigned char smraw_[];
     T* bufV = reinterpret_cast<T*>(smraw_);
-    constexpr int TC = WPB * (32 / LPR) * (LPR == 32 ? 2 : 1);   // == col_tile<LPR>() of the launcher
+    constexpr int TC = WPB * (32 / LPR) * (LPR == 32 ? 2 : 1);   // == col_tile<WPB, LPR>() of the launcher
     T* bufB = bufV + TC * LP;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;

@@ -16,15 +16,17 @@ template <typename T> struct PlaneBwdArgs;
 
 // (E samples per lane, LPR lanes per line) chosen for a line length n.
 struct Geo { int E, LPR; };
-// TVP_GEO16=1 (environment, A/B): fp32 lines of 129..224 samples go to half-warp
-// groups of 14 samples per lane (two lines per warp) instead of one warp of 7 per
-// lane -- the per-iteration scan / vote overhead is shared by twice the samples.
+// TVP_GEO16=1 (default; environment 0 for A/B): fp32 lines of 129..224 samples go to
+// half-warp groups of 14 samples per lane (two lines per warp) instead of one warp of 7
+// per lane, and 65..128 samples to half-warp groups of 8 instead of one warp of 4 --
+// the per-iteration scan / vote overhead is shared by twice the samples.
 #ifndef TVP_GEO16_DEFAULT
 #define TVP_GEO16_DEFAULT 1
 #endif
 int geo16_knob();
 inline Geo pick_geo(int64_t n, int esz = 8) {
     if (esz == 4 && n > 128 && n <= 224 && geo16_knob()) return {14, 16};
+    if (esz == 4 && n > 64 && n <= 128 && geo16_knob()) return {8, 16};
     if (n <= 16) return {2, 8};
     if (n <= 32) return {4, 8};
     if (n <= 56) return {7, 8};

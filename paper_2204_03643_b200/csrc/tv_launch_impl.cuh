@@ -43,7 +43,8 @@ static int persistent_grid(K kern, int threads, size_t smem, int64_t work_blocks
         Geo g_ = pick_geo(n, (int)sizeof(T));                                  \
         if (g_.LPR == 16) {                                                    \
             if constexpr (sizeof(T) == 4) {                                    \
-                constexpr int E_ = 14, L_ = 16; __VA_ARGS__;                   \
+                if (g_.E == 14) { constexpr int E_ = 14, L_ = 16; __VA_ARGS__; }   \
+                else { constexpr int E_ = 8, L_ = 16; __VA_ARGS__; }           \
             }                                                                  \
         } else if (g_.LPR == 8) {                                              \
             switch (g_.E) {                                                    \
