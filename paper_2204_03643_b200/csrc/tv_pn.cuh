@@ -450,8 +450,11 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
 #endif
         if (run) ++it;
         if (run && ok) { conv = true; run = false; }
-        // one line per group and warp: a fast-mode convergence leaves xhat in w
-        if ((LPR == 32) && !lsmode && !C.uany(run)) {
+        // every line of the warp has stopped after a fast-mode step: this step's P3 left
+        // each line's candidate in w (a line that stopped earlier recomputes the same
+        // candidate bitwise: its bound set is frozen and xhat reads u only on bound
+        // edges), so the final candidate pass is not needed
+        if (!lsmode && !C.uany(run)) {
             fin_direct = true;
             break;
         }
