@@ -296,11 +296,13 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         //   xhat = (sum_y - u_{a-1} + u_{b-1}) / len ;  s carries sum_y - u_{a-1}.
         const bool upd = run && !first && !fin;
         const uint32_t keep = upd ? pin : bnd;
-        T uprev, unext;
-        C.template prev_next<0>(u[E - 1], u[0], uprev, unext);
-        // (a) outward-gradient bits at the bound (predicate -> one OR per sample)
+        T uprev = T(0), unext = T(0);
+        // (a) outward-gradient bits at the bound (predicate -> one OR per sample); not
+        // needed when no line of the warp updates its bound set (the first step from
+        // the initial set, the final candidate pass): outb would be 0 there
         uint32_t outb = 0;
-        {
+        if (C.uany(upd)) {
+            C.template prev_next<0>(u[E - 1], u[0], uprev, unext);
             T xk = y[0] + u[0] - uprev;
 #pragma unroll
             for (int k = 0; k < E; ++k) {
