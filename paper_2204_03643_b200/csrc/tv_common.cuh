@@ -89,6 +89,16 @@ __device__ __forceinline__ uint32_t edge_code(T xl, T xr, bool lam_zero) {
     return xr > xl ? CODE_UP : (xr < xl ? CODE_DOWN : (lam_zero ? CODE_BOUNDARY : CODE_FUSED));
 }
 
+// Spread bits 0..15 of x to the even positions 0, 2, ..., 30 (inverse of compact_even).
+__device__ __forceinline__ uint32_t spread_even(uint32_t x) {
+    x &= 0x0000ffffu;
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    x = (x | (x << 4)) & 0x0f0f0f0fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+
 // Gather the even bits of x (bits 0, 2, ..., 30) into bits 0..15.
 __device__ __forceinline__ uint32_t compact_even(uint32_t x) {
     x &= 0x55555555u;

@@ -442,12 +442,29 @@ k_row_fwd_w(RowFwdArgs<T> a) {
             // 2-bit codes of the lane's edges i0 .. i0+E-1 (edge e between samples e, e+1)
             const T wnext = C.template next<11>(w[0]);
             uint32_t word = 0;
+            if constexpr (E == 16 && !PE) {
+                // bit-parallel: up / down jump bits per edge, then spread to the 2-bit codes
+                uint32_t up = 0u, dn = 0u;
 #pragma unroll
-            for (int k = 0; k < E; ++k) {
-                const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnext;
-                const bool lz = PE ? !(lam.e[PE ? k : 0] > T(0)) : !(lam.r > T(0));
-                const uint32_t code = (i0 + k < n - 1) ? edge_code(w[k], xr, lz) : 0u;
-                word |= code << (2 * ((i0 + k) & 15));
+                for (int k = 0; k < E; ++k) {
+                    const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnext;
+                    up |= (xr > w[k] ? 1u : 0u) << k;
+                    dn |= (xr < w[k] ? 1u : 0u) << k;
+                }
+                const int ne = n - 1 - i0;                        // this lane's edges < n - 1
+                const uint32_t vm = ne >= 16 ? 0xffffu : (ne <= 0 ? 0u : ((1u << ne) - 1u));
+                up &= vm;
+                dn &= vm;
+                const uint32_t bz = (lam.r > T(0)) ? 0u : (vm & ~(up | dn));   // lam = 0: boundary
+                word = spread_even(up | bz) | (spread_even(dn | bz) << 1);
+            } else {
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnext;
+                    const bool lz = PE ? !(lam.e[PE ? k : 0] > T(0)) : !(lam.r > T(0));
+                    const uint32_t code = (i0 + k < n - 1) ? edge_code(w[k], xr, lz) : 0u;
+                    word |= code << (2 * ((i0 + k) & 15));
+                }
             }
             if (E < 16) {               // 16 / E lanes share one word
 #pragma unroll
