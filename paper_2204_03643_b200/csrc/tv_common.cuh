@@ -99,6 +99,29 @@ __device__ __forceinline__ uint32_t spread_even(uint32_t x) {
     return x;
 }
 
+// 2-bit codes of a lane's E <= 16 edges e0 .. e0 + E - 1 (edge k between samples k and
+// k + 1 of the lane, x_r of the last one from the next lane), bit-parallel: jump bits,
+// masked to the line's edges (< nedge), spread to codes at bits 2k; boundary code where
+// lam = 0 and the values are equal.  Same codes as edge_code per edge.
+template <typename T, int E>
+__device__ __forceinline__ uint32_t lane_codes(const T (&w)[E], T wnext, int e0, int nedge, bool lam_zero) {
+    static_assert(E <= 16, "one word of codes per lane");
+    uint32_t up = 0u, dn = 0u;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnext;
+        up |= (xr > w[k] ? 1u : 0u) << k;
+        dn |= (xr < w[k] ? 1u : 0u) << k;
+    }
+    constexpr uint32_t allm = (E == 32) ? 0xffffffffu : ((1u << (E & 31)) - 1u);
+    const int ne = nedge - e0;
+    const uint32_t vm = ne >= E ? allm : (ne <= 0 ? 0u : ((1u << ne) - 1u));
+    up &= vm;
+    dn &= vm;
+    const uint32_t bz = lam_zero ? (vm & ~(up | dn)) : 0u;
+    return spread_even(up | bz) | (spread_even(dn | bz) << 1);
+}
+
 // Gather the even bits of x (bits 0, 2, ..., 30) into bits 0..15.
 __device__ __forceinline__ uint32_t compact_even(uint32_t x) {
     x &= 0x55555555u;

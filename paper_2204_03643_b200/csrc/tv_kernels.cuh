@@ -338,13 +338,20 @@ k_row_fwd(RowFwdArgs<T> a) {
             const int e0 = l * E;
             const int wlo = e0 >> 4;
             uint32_t clo = 0u, chi = 0u;
+            if constexpr (E <= 16 && !PE) {
+                const uint32_t code = lane_codes<T, E>(w, wnx, e0, n - 1, !(lam.r > T(0)));
+                const int sh = 2 * (e0 & 15);
+                clo = code << sh;
+                chi = sh ? (code >> (32 - sh)) : 0u;
+            } else {
 #pragma unroll
-            for (int k = 0; k < E; ++k) {
-                const int e = e0 + k;
-                const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnx;
-                const bool lz = PE ? !(lam.e[PE ? k : 0] > T(0)) : !(lam.r > T(0));
-                const uint32_t code = (e < n - 1) ? edge_code(w[k], xr, lz) << (2 * (e & 15)) : 0u;
-                if ((e >> 4) == wlo) clo |= code; else chi |= code;
+                for (int k = 0; k < E; ++k) {
+                    const int e = e0 + k;
+                    const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnx;
+                    const bool lz = PE ? !(lam.e[PE ? k : 0] > T(0)) : !(lam.r > T(0));
+                    const uint32_t code = (e < n - 1) ? edge_code(w[k], xr, lz) << (2 * (e & 15)) : 0u;
+                    if ((e >> 4) == wlo) clo |= code; else chi |= code;
+                }
             }
             __syncwarp();
             if (valid && clo) atomicOr(&mwb[grp * (32 / G) + wlo], clo);
@@ -443,20 +450,7 @@ k_row_fwd_w(RowFwdArgs<T> a) {
             const T wnext = C.template next<11>(w[0]);
             uint32_t word = 0;
             if constexpr (E == 16 && !PE) {
-                // bit-parallel: up / down jump bits per edge, then spread to the 2-bit codes
-                uint32_t up = 0u, dn = 0u;
-#pragma unroll
-                for (int k = 0; k < E; ++k) {
-                    const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnext;
-                    up |= (xr > w[k] ? 1u : 0u) << k;
-                    dn |= (xr < w[k] ? 1u : 0u) << k;
-                }
-                const int ne = n - 1 - i0;                        // this lane's edges < n - 1
-                const uint32_t vm = ne >= 16 ? 0xffffu : (ne <= 0 ? 0u : ((1u << ne) - 1u));
-                up &= vm;
-                dn &= vm;
-                const uint32_t bz = (lam.r > T(0)) ? 0u : (vm & ~(up | dn));   // lam = 0: boundary
-                word = spread_even(up | bz) | (spread_even(dn | bz) << 1);
+                word = lane_codes<T, E>(w, wnext, i0, n - 1, !(lam.r > T(0)));   // bit-parallel
             } else {
 #pragma unroll
                 for (int k = 0; k < E; ++k) {
@@ -735,12 +729,19 @@ k_col_fwd(ColFwdArgs<T> a) {
                 const int wlo = e0 >> 4;
                 const bool lz = !(lamp > T(0));
                 uint32_t clo = 0u, chi = 0u;
+                if constexpr (E <= 16) {
+                    const uint32_t code = lane_codes<T, E>(w, wnx, e0, H - 1, lz);
+                    const int sh = 2 * (e0 & 15);
+                    clo = code << sh;
+                    chi = sh ? (code >> (32 - sh)) : 0u;
+                } else {
 #pragma unroll
-                for (int k = 0; k < E; ++k) {
-                    const int e = e0 + k;
-                    const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnx;
-                    const uint32_t code = (e < H - 1) ? edge_code(w[k], xr, lz) << (2 * (e & 15)) : 0u;
-                    if ((e >> 4) == wlo) clo |= code; else chi |= code;
+                    for (int k = 0; k < E; ++k) {
+                        const int e = e0 + k;
+                        const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnx;
+                        const uint32_t code = (e < H - 1) ? edge_code(w[k], xr, lz) << (2 * (e & 15)) : 0u;
+                        if ((e >> 4) == wlo) clo |= code; else chi |= code;
+                    }
                 }
                 __syncwarp();
                 if (clo) atomicOr(&gw[wlo], clo);
