@@ -103,10 +103,13 @@ __device__ __forceinline__ uint32_t spread_even(uint32_t x) {
 // k + 1 of the lane, x_r of the last one from the next lane), bit-parallel: jump bits,
 // masked to the line's edges (< nedge), spread to codes at bits 2k; boundary code where
 // lam = 0 and the values are equal.  Same codes as edge_code per edge.
+// up / dn return the lanes' jump bits (edges coded CODE_UP / CODE_DOWN).
 template <typename T, int E>
-__device__ __forceinline__ uint32_t lane_codes(const T (&w)[E], T wnext, int e0, int nedge, bool lam_zero) {
+__device__ __forceinline__ uint32_t lane_codes(const T (&w)[E], T wnext, int e0, int nedge, bool lam_zero,
+                                               uint32_t& up, uint32_t& dn) {
     static_assert(E <= 16, "one word of codes per lane");
-    uint32_t up = 0u, dn = 0u;
+    up = 0u;
+    dn = 0u;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnext;
@@ -120,6 +123,11 @@ __device__ __forceinline__ uint32_t lane_codes(const T (&w)[E], T wnext, int e0,
     dn &= vm;
     const uint32_t bz = lam_zero ? (vm & ~(up | dn)) : 0u;
     return spread_even(up | bz) | (spread_even(dn | bz) << 1);
+}
+template <typename T, int E>
+__device__ __forceinline__ uint32_t lane_codes(const T (&w)[E], T wnext, int e0, int nedge, bool lam_zero) {
+    uint32_t up, dn;
+    return lane_codes<T, E>(w, wnext, e0, nedge, lam_zero, up, dn);
 }
 
 // Gather the even bits of x (bits 0, 2, ..., 30) into bits 0..15.

@@ -1101,17 +1101,11 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
                 const int st = solve_line<T, ER, LPR, 1, false>(y, w, lm, W, valid, wp0, wn0, Cm);
                 // codes of the lane's edges: next pass's warm bits and the saved mask
                 const T wnx = shdn<LPR>(w[0], 1);
-                uint32_t up = 0u, dn = 0u, clo = 0u, chi = 0u;
+                uint32_t up, dn;
                 const int e0 = l * ER, wlo = e0 >> 4;
-#pragma unroll
-                for (int q = 0; q < ER; ++q) {
-                    const int e = e0 + q;
-                    const T xr = (q + 1 < ER) ? w[(q + 1 < ER) ? q + 1 : q] : wnx;
-                    const uint32_t code = (e < W - 1) ? edge_code(w[q], xr, lz) : 0u;
-                    up |= (code == CODE_UP ? 1u : 0u) << q;
-                    dn |= (code == CODE_DOWN ? 1u : 0u) << q;
-                    if ((e >> 4) == wlo) clo |= code << (2 * (e & 15)); else chi |= code << (2 * (e & 15));
-                }
+                const uint32_t code = lane_codes<T, ER>(w, wnx, e0, W - 1, lz, up, dn);   // bit-parallel
+                const int sh = 2 * (e0 & 15);
+                const uint32_t clo = code << sh, chi = sh ? (code >> (32 - sh)) : 0u;
                 wrp[t * 32 + lane] = up;
                 wrn[t * 32 + lane] = dn;
                 if (valid) {
@@ -1156,17 +1150,11 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
                 lm.r = lamp;
                 const int st = solve_line<T, EC, LPR, 1, false>(y, w, lm, H, valid, wp0, wn0, Cm);
                 const T wnx = shdn<LPR>(w[0], 1);
-                uint32_t up = 0u, dn = 0u, clo = 0u, chi = 0u;
+                uint32_t up, dn;
                 const int e0 = l * EC, wlo = e0 >> 4;
-#pragma unroll
-                for (int q = 0; q < EC; ++q) {
-                    const int e = e0 + q;
-                    const T xr = (q + 1 < EC) ? w[(q + 1 < EC) ? q + 1 : q] : wnx;
-                    const uint32_t code = (e < H - 1) ? edge_code(w[q], xr, lz) : 0u;
-                    up |= (code == CODE_UP ? 1u : 0u) << q;
-                    dn |= (code == CODE_DOWN ? 1u : 0u) << q;
-                    if ((e >> 4) == wlo) clo |= code << (2 * (e & 15)); else chi |= code << (2 * (e & 15));
-                }
+                const uint32_t code = lane_codes<T, EC>(w, wnx, e0, H - 1, lz, up, dn);   // bit-parallel
+                const int sh = 2 * (e0 & 15);
+                const uint32_t clo = code << sh, chi = sh ? (code >> (32 - sh)) : 0u;
                 wcp[t * 32 + lane] = up;
                 wcn[t * 32 + lane] = dn;
                 if (valid) {
