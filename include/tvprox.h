@@ -47,15 +47,64 @@ typedef enum {
 
 typedef enum { TVP_OK = 0, TVP_EINVAL = 1, TVP_EUNSUPPORTED = 2, TVP_ECUDA = 3 } tvp_status_t;
 
-/* row_iters codes written by the forward calls */
+/* row_iters codes written by the forward calls.  A value >= 0 is
+ *   bits 0..15   PN iterations,
+ *   bit  16      TVP_ITERS_STALL_FLAG: accepted at a rounding-level fixed point,
+ *   bits 20..27  line-search passes (function evaluations of the projected line
+ *                search of P:188, saturating at 255; 0 when every step was a full
+ *                Newton step), see tvp_options_t.
+ * (TVP_ITERS_COUNT / TVP_ITERS_LS extract the fields.) */
 #define TVP_ITERS_NOT_CONVERGED (-1)   /* max iterations hit; x = y - D^T u (feasible dual) */
 #define TVP_ITERS_NONFINITE     (-2)   /* NaN/Inf in the row (or its lam): row set to NaN  */
 #define TVP_ITERS_STALL_FLAG    (1 << 16) /* or-ed into a count: accepted at a rounding-level fixed point */
+#define TVP_ITERS_COUNT(v)      ((v) & 0xffff)
+#define TVP_ITERS_LS(v)         (((v) >> 20) & 0xff)
 
-/* Performance switch of the 2D forward: planes with 32 < H, W <= 64
- * run all K Dykstra passes on chip (one CTA per plane, state in shared memory);
- * the result is bitwise the staged path's.  Default on (env TVP_FUSED2D=0 turns it
- * off); returns the previous setting.  Not thread-safe against concurrent calls. */
+/* ----------------------------------------------------- per-call options --- */
+/*
+ * Options of the *_ex calls (NULL = defaults; tvp_options_default fills them).
+ * Everything here is per call: no library state is read or written except the
+ * calling thread's fused-2D default (tvp_set_fused2d).
+ *
+ *   fused2d      2D only.  -1: the calling thread's default (initially on, unless
+ *                the environment has TVP_FUSED2D=0); 0: staged row / column passes
+ *                through HBM; 1: planes with 32 < H, W <= 64 run all K Dykstra
+ *                passes on chip.  The output, saved masks and
+ *                gradients are bitwise the same either way.
+ *   line_search  Globalisation of the projected Newton step:
+ *                TVP_LS_BACKTRACK (default) = projected Armijo search with
+ *                quadratic-interpolation backtracking ("only iterates a few times",
+ *                P:188); TVP_LS_PARALLEL = the parallel multi-step-size search P:188
+ *                compares it with (alpha, alpha/2, alpha/4, alpha/8 per pass, the
+ *                largest Armijo-accepted one taken).
+ *   ls_after     From PN iteration ls_after on, a step whose full Newton point
+ *                leaves the box runs the line search; before it, such a step is the
+ *                projected full step.  0 = default (12); 1 or 2 = the search guards
+ *                every such step (the paper's method as written).  The prox, and so
+ *                the result up to rounding, does not depend on it; iteration counts do.
+ *   diag         nullable device int32[4], ACCUMULATED by the call (zero it first):
+ *                [0] lines solved, [1] lines that ran the line search, [2] line-search
+ *                passes, [3] lines accepted at a stall (integer atomics: deterministic).
+ *   iter_hist    nullable device int32[passes][TVP_HIST_BINS], ACCUMULATED: number of
+ *                lines by PN-iteration count (last bin: not converged or non-finite);
+ *                passes = 1 for 1D, 2*iters for 2D (row pass k at 2(k-1), column pass
+ *                k at 2(k-1)+1).
+ * Errors: TVP_EINVAL for fused2d not in {-1,0,1}, line_search not a
+ * tvp_line_search_t, ls_after < 0.
+ */
+typedef enum { TVP_LS_BACKTRACK = 0, TVP_LS_PARALLEL = 1 } tvp_line_search_t;
+#define TVP_HIST_BINS 128
+typedef struct tvp_options {
+    int fused2d;
+    int line_search;
+    int ls_after;
+    int32_t *diag;
+    int32_t *iter_hist;
+} tvp_options_t;
+void tvp_options_default(tvp_options_t *opts);
+
+/* The calling thread's default for tvp_options_t.fused2d = -1 (thread-local; initially
+ * on unless TVP_FUSED2D=0 in the environment).  Returns the previous setting. */
 int tvp_set_fused2d(int enable);
 
 /* Longest 2D line (W and H) the register-resident solver takes (1024). */
@@ -105,6 +154,16 @@ tvp_status_t tv1d_prox_fwd_warm(tvp_dtype_t dt, const void *y, void *x,
                                 const void *lam, tvp_lam_mode_t lm, double lam_scalar,
                                 const uint32_t *mask_in, uint32_t *mask_out,
                                 int32_t *row_iters, tvp_stream_t stream);
+
+/*
+ * tv1d_prox_fwd_ex -- tv1d_prox_fwd (mask_in == NULL) or tv1d_prox_fwd_warm
+ * (mask_in != NULL) with per-call options (tvp_options_t; NULL = defaults).
+ */
+tvp_status_t tv1d_prox_fwd_ex(tvp_dtype_t dt, const void *y, void *x,
+                              int64_t batch, int64_t n, int64_t stride,
+                              const void *lam, tvp_lam_mode_t lm, double lam_scalar,
+                              const uint32_t *mask_in, uint32_t *mask_out, int32_t *row_iters,
+                              const tvp_options_t *opts, tvp_stream_t stream);
 
 /* Workspace of tv1d_prox_bwd in bytes (nonzero only for TVP_LAM_SCALAR). */
 size_t tv1d_bwd_workspace_bytes(tvp_dtype_t dt, int64_t batch, tvp_lam_mode_t lm);
@@ -174,6 +233,19 @@ tvp_status_t tv2d_prox_bwd(tvp_dtype_t dt, const void *grad_Y, const void *saved
                            int64_t N, int64_t C, int64_t H, int64_t W,
                            tvp_lam_mode_t lm, int iters, void *workspace,
                            tvp_stream_t stream);
+
+/* tv2d_prox_fwd / tv2d_prox_bwd with per-call options (tvp_options_t; NULL =
+ * defaults).  The backward reads only opts->fused2d. */
+tvp_status_t tv2d_prox_fwd_ex(tvp_dtype_t dt, const void *X, void *Y,
+                              int64_t N, int64_t C, int64_t H, int64_t W,
+                              const void *lam, tvp_lam_mode_t lm, double lam_scalar, int iters,
+                              void *saved, void *workspace, int32_t *line_iters,
+                              const tvp_options_t *opts, tvp_stream_t stream);
+tvp_status_t tv2d_prox_bwd_ex(tvp_dtype_t dt, const void *grad_Y, const void *saved,
+                              void *grad_X, void *grad_lam,
+                              int64_t N, int64_t C, int64_t H, int64_t W,
+                              tvp_lam_mode_t lm, int iters, void *workspace,
+                              const tvp_options_t *opts, tvp_stream_t stream);
 
 /* ----------------------------------------------------- TV layer (NEXT f1) --- */
 /*

@@ -61,6 +61,8 @@ def _get():
                                                i8p, i8p, i8p, i8p, ctypes.c_int]
             lib.tvref_bwd2d_batch.argtypes = [i64, i64, i64, ctypes.c_int, i8p, i8p, i8p, i8p,
                                               dp, dp, dp, ctypes.c_int]
+            lib.tvref_prox2d_batch_ex.argtypes = [i64, i64, i64, dp, dp, ctypes.c_int, dp,
+                                                  i8p, i8p, i8p, i8p, dp, dp, ctypes.c_int]
             _lib = lib
     return _lib
 
@@ -181,8 +183,9 @@ def bwd2d(segs, G, K):
     return GX, float(gl[0])
 
 
-def prox2d_batch(X, lam, K, nthreads=1, with_codes=True):
-    """Planes X [P, H, W], lam [P].  Returns (Y, segs)."""
+def prox2d_batch(X, lam, K, nthreads=1, with_codes=True, with_jumps=False):
+    """Planes X [P, H, W], lam [P].  Returns (Y, segs), or (Y, segs, (rjmp, cjmp)) with
+    with_jumps: the jumps out[e+1] - out[e] of every 1D pass output, [P][K][lines][n-1]."""
     X = _f64(X)
     P, H, W = X.shape
     lam = _f64(lam)
@@ -194,10 +197,14 @@ def prox2d_batch(X, lam, K, nthreads=1, with_codes=True):
         cs = np.zeros_like(cb)
     else:
         rb = rs = cb = cs = None
-    st = _get().tvref_prox2d_batch(P, H, W, _p(X), _p(lam), int(K), _p(Y), _p(rb), _p(rs),
-                                   _p(cb), _p(cs), int(nthreads))
+    rj = np.zeros((P, K, H, max(W - 1, 0))) if with_jumps else None
+    cj = np.zeros((P, K, W, max(H - 1, 0))) if with_jumps else None
+    st = _get().tvref_prox2d_batch_ex(P, H, W, _p(X), _p(lam), int(K), _p(Y), _p(rb), _p(rs),
+                                      _p(cb), _p(cs), _p(rj), _p(cj), int(nthreads))
     if st:
         raise MemoryError("tvref prox2d_batch failed")
+    if with_jumps:
+        return Y, (rb, rs, cb, cs), (rj, cj)
     return Y, (rb, rs, cb, cs)
 
 

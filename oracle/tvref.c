@@ -221,9 +221,12 @@ void tvref_bwd1d(int64_t n, const int8_t *brk, const int8_t *sgn, const double *
 /*   return Y(K+1)                                                          */
 /* Segmentations of every 1D call are returned (nullable) for the backward: */
 /*   rbrk/rsgn: [K][H][W-1]   cbrk/csgn: [K][W][H-1]                        */
+/* and (nullable, tvref_prox2d_ex) the jumps out[e+1] - out[e] of every 1D   */
+/* call's output, same layout (the parity tests' mask audit, reading O13).   */
 /* ------------------------------------------------------------------------ */
-int tvref_prox2d(int64_t H, int64_t W, const double *X, double lam, int K,
-                 double *Yout, int8_t *rbrk, int8_t *rsgn, int8_t *cbrk, int8_t *csgn)
+int tvref_prox2d_ex(int64_t H, int64_t W, const double *X, double lam, int K,
+                    double *Yout, int8_t *rbrk, int8_t *rsgn, int8_t *cbrk, int8_t *csgn,
+                    double *rjmp, double *cjmp)
 {
     int64_t HW = H * W;
     int64_t mx = H > W ? H : W;
@@ -251,6 +254,7 @@ int tvref_prox2d(int64_t H, int64_t W, const double *X, double lam, int K,
                 int64_t o = ((int64_t)k * H + m) * (W - 1) + e;
                 if (rbrk) rbrk[o] = tb[e];
                 if (rsgn) rsgn[o] = ts[e];
+                if (rjmp) rjmp[o] = out[e + 1] - out[e];
             }
         }
         for (int64_t i = 0; i < HW; ++i) P[i] = P[i] + Y[i] - Z[i];
@@ -264,6 +268,7 @@ int tvref_prox2d(int64_t H, int64_t W, const double *X, double lam, int K,
                 int64_t o = ((int64_t)k * W + c) * (H - 1) + e;
                 if (cbrk) cbrk[o] = tb[e];
                 if (csgn) csgn[o] = ts[e];
+                if (cjmp) cjmp[o] = out[e + 1] - out[e];
             }
         }
         for (int64_t i = 0; i < HW; ++i) Q[i] = Q[i] + Z[i] - Y[i];
@@ -271,6 +276,12 @@ int tvref_prox2d(int64_t H, int64_t W, const double *X, double lam, int K,
     memcpy(Yout, Y, sizeof(double) * (size_t)HW);
     free(Y); free(Z); free(P); free(Q); free(in); free(out); free(tb); free(ts);
     return 0;
+}
+
+int tvref_prox2d(int64_t H, int64_t W, const double *X, double lam, int K,
+                 double *Yout, int8_t *rbrk, int8_t *rsgn, int8_t *cbrk, int8_t *csgn)
+{
+    return tvref_prox2d_ex(H, W, X, lam, K, Yout, rbrk, rsgn, cbrk, csgn, NULL, NULL);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -352,6 +363,7 @@ typedef struct {
     int K;
     const double *in, *lam, *g;
     double *out, *out2;
+    double *j1, *j2;
     int8_t *b1, *s1, *b2, *s2;
     const int8_t *cb1, *cs1, *cb2, *cs2;
     int per_edge;
@@ -380,9 +392,10 @@ static void *tvref_worker(void *arg)
             int64_t HW = j->H * j->W;
             int64_t rs = (int64_t)j->K * j->H * (j->W - 1);
             int64_t cs = (int64_t)j->K * j->W * (j->H - 1);
-            int st = tvref_prox2d(j->H, j->W, j->in + r * HW, j->lam[r], j->K, j->out + r * HW,
-                                  j->b1 ? j->b1 + r * rs : NULL, j->s1 ? j->s1 + r * rs : NULL,
-                                  j->b2 ? j->b2 + r * cs : NULL, j->s2 ? j->s2 + r * cs : NULL);
+            int st = tvref_prox2d_ex(j->H, j->W, j->in + r * HW, j->lam[r], j->K, j->out + r * HW,
+                                     j->b1 ? j->b1 + r * rs : NULL, j->s1 ? j->s1 + r * rs : NULL,
+                                     j->b2 ? j->b2 + r * cs : NULL, j->s2 ? j->s2 + r * cs : NULL,
+                                     j->j1 ? j->j1 + r * rs : NULL, j->j2 ? j->j2 + r * cs : NULL);
             if (st) j->status = st;
         } else {
             int64_t HW = j->H * j->W;
@@ -438,14 +451,21 @@ int tvref_bwd1d_batch(int64_t batch, int64_t n, const int8_t *brk, const int8_t 
     return tvref_run(j, batch, nthreads);
 }
 
+int tvref_prox2d_batch_ex(int64_t planes, int64_t H, int64_t W, const double *X, const double *lam,
+                          int K, double *Y, int8_t *rbrk, int8_t *rsgn, int8_t *cbrk, int8_t *csgn,
+                          double *rjmp, double *cjmp, int nthreads)
+{
+    tvref_job_t j; memset(&j, 0, sizeof j);
+    j.kind = 2; j.H = H; j.W = W; j.K = K; j.in = X; j.lam = lam; j.out = Y;
+    j.b1 = rbrk; j.s1 = rsgn; j.b2 = cbrk; j.s2 = csgn; j.j1 = rjmp; j.j2 = cjmp;
+    return tvref_run(j, planes, nthreads);
+}
+
 int tvref_prox2d_batch(int64_t planes, int64_t H, int64_t W, const double *X, const double *lam,
                        int K, double *Y, int8_t *rbrk, int8_t *rsgn, int8_t *cbrk, int8_t *csgn,
                        int nthreads)
 {
-    tvref_job_t j; memset(&j, 0, sizeof j);
-    j.kind = 2; j.H = H; j.W = W; j.K = K; j.in = X; j.lam = lam; j.out = Y;
-    j.b1 = rbrk; j.s1 = rsgn; j.b2 = cbrk; j.s2 = csgn;
-    return tvref_run(j, planes, nthreads);
+    return tvref_prox2d_batch_ex(planes, H, W, X, lam, K, Y, rbrk, rsgn, cbrk, csgn, NULL, NULL, nthreads);
 }
 
 int tvref_bwd2d_batch(int64_t planes, int64_t H, int64_t W, int K,

@@ -16,12 +16,31 @@ TVP_F32, TVP_F64 = 0, 1
 LAM_SCALAR, LAM_PER_ROW, LAM_PER_EDGE, LAM_PER_CHANNEL, LAM_PER_PLANE = 0, 1, 2, 3, 4
 TVP_OK, TVP_EINVAL, TVP_EUNSUPPORTED, TVP_ECUDA = 0, 1, 2, 3
 ITERS_NOT_CONVERGED, ITERS_NONFINITE, ITERS_STALL_FLAG = -1, -2, 1 << 16
+LS_BACKTRACK, LS_PARALLEL = 0, 1
+HIST_BINS = 128
+
+
+def iters_count(v):
+    """PN iterations of a row_iters value >= 0 (bits 0..15)."""
+    return v & 0xFFFF
+
+
+def iters_ls(v):
+    """Line-search passes of a row_iters value >= 0 (bits 20..27)."""
+    return (v >> 20) & 0xFF
+
+
+class Options(ctypes.Structure):
+    """tvp_options_t (include/tvprox.h): per-call options of the *_ex entry points."""
+    _fields_ = [("fused2d", ctypes.c_int), ("line_search", ctypes.c_int), ("ls_after", ctypes.c_int),
+                ("diag", ctypes.c_void_p), ("iter_hist", ctypes.c_void_p)]
 
 # every symbol include/tvprox.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "tvp_max_line", "tvp_max_line_1d", "tvp_set_fused2d", "tv1d_mask_words", "tv1d_prox_fwd", "tv1d_prox_fwd_warm", "tv1d_bwd_workspace_bytes",
+    "tvp_max_line", "tvp_max_line_1d", "tvp_set_fused2d", "tvp_options_default",
+    "tv1d_mask_words", "tv1d_prox_fwd", "tv1d_prox_fwd_warm", "tv1d_prox_fwd_ex", "tv1d_bwd_workspace_bytes",
     "tv1d_prox_bwd",
-    "tv2d_saved_bytes", "tv2d_workspace_bytes", "tv2d_prox_fwd", "tv2d_prox_bwd",
+    "tv2d_saved_bytes", "tv2d_workspace_bytes", "tv2d_prox_fwd", "tv2d_prox_bwd", "tv2d_prox_fwd_ex", "tv2d_prox_bwd_ex",
     "tv2d_lines_fwd", "tv2d_lines_workspace_bytes", "tv2d_lines_bwd",
     "tvp_softplus_fwd", "tvp_softplus_bwd", "tvp_axpby",
     "tvp_status_string", "tvp_last_error", "tvp_version", "tvp_launch_count",
@@ -67,6 +86,16 @@ def load(path: str = LIB_PATH):
         _sig(lib, "tv1d_prox_fwd", "restype", i32)
         _sig(lib, "tv1d_prox_fwd_warm", "argtypes", [i32, vp, vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp, vp])
         _sig(lib, "tv1d_prox_fwd_warm", "restype", i32)
+        op = ctypes.POINTER(Options)
+        _sig(lib, "tvp_options_default", "argtypes", [op])
+        _sig(lib, "tvp_options_default", "restype", None)
+        _sig(lib, "tv1d_prox_fwd_ex", "argtypes", [i32, vp, vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp, op, vp])
+        _sig(lib, "tv1d_prox_fwd_ex", "restype", i32)
+        _sig(lib, "tv2d_prox_fwd_ex", "argtypes", [i32, vp, vp, i64, i64, i64, i64, vp, i32, dbl, i32, vp, vp, vp, op,
+                                                   vp])
+        _sig(lib, "tv2d_prox_fwd_ex", "restype", i32)
+        _sig(lib, "tv2d_prox_bwd_ex", "argtypes", [i32, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, vp, op, vp])
+        _sig(lib, "tv2d_prox_bwd_ex", "restype", i32)
         _sig(lib, "tv1d_bwd_workspace_bytes", "argtypes", [i32, i64, i32])
         _sig(lib, "tv1d_bwd_workspace_bytes", "restype", u64)
         _sig(lib, "tv1d_prox_bwd", "argtypes", [i32, vp, vp, vp, vp, i64, i64, i64, i32, vp, vp])

@@ -1,0 +1,5 @@
+// Instantiation unit: coarse pre-pass, backward, reduction and elementwise launchers, double (sm_100a).
+#include "tv_launch_impl.cuh"
+namespace tvp {
+TVP_INST_BWD(double)
+}

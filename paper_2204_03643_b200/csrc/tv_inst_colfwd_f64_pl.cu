@@ -1,0 +1,6 @@
+// Instantiation unit: column-forward and fused-plane-forward launchers, double, LSP=true (sm_100a).
+#include "tv_launch_impl.cuh"
+namespace tvp {
+TVP_INST_COLFWD(double, true)
+TVP_INST_PLANE(double, true)
+}

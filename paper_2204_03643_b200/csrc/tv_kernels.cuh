@@ -36,6 +36,9 @@ struct RowFwdArgs {
     int32_t* row_iters;        // nullable
     int32_t* iters_max;        // nullable (2D diagnostics)
     int coarse;                // cold solve: coarse initial bound set (coarse_init)
+    int ls_after;              // PN iteration from which the projected line search runs (a-7)
+    int32_t* diag;             // nullable: accumulated line counters (line_diag)
+    int32_t* hist;             // nullable: [kHistBins] lines per PN-iteration count
 };
 
 template <typename T>
@@ -56,6 +59,9 @@ struct ColFwdArgs {
     int TC;
     int32_t* iters_max;
     int coarse;              // cold solve: coarse initial bound set (coarse_init)
+    int ls_after;            // PN iteration from which the projected line search runs (a-7)
+    int32_t* diag;           // nullable: accumulated line counters (line_diag)
+    int32_t* hist;           // nullable: [kHistBins] lines per PN-iteration count
 };
 
 template <typename T>
@@ -151,11 +157,11 @@ __device__ __forceinline__ void smem_to_regs(const T* buf, int l, T (&y)[E]) {
 // Solve one line held by this lane group: centring, pinning, non-finite
 // detection, PN solve.  Writes the uncentred output into `w` and returns the
 // status (row_iters code).
-template <typename T, int E, int LPR, int WPL, bool PE>
+template <typename T, int E, int LPR, int WPL, bool PE, bool LSP = false>
 __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& lam, int n,
                                           bool valid, uint32_t warm_pos, uint32_t warm_neg,
                                           const Comm<T, LPR, WPL>& C, bool coarse = false,
-                                          T* xb = nullptr) {
+                                          T* xb = nullptr, int ls_after = kLsAfterDefault) {
     const int ll = C.w * LPR + C.l;           // line lane
     constexpr uint32_t allm = (E == 32) ? 0xffffffffu : ((1u << (E & 31)) - 1u);
     uint32_t pin;
@@ -206,11 +212,31 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
         warm_neg |= cn;
     }
     T u[E];
-    int st = pn_solve<T, E, LPR, WPL, PE>(y, u, w, pin, warm_pos, warm_neg, lam, C, active);
+    int lsp = 0;
+    int st = pn_solve<T, E, LPR, WPL, PE, LSP>(y, u, w, pin, warm_pos, warm_neg, lam, C, active, ls_after, lsp);
 #pragma unroll
     for (int k = 0; k < E; ++k) w[k] = active ? w[k] + mean : (bad ? nan_<T>() : y[k]);
     if (!active) st = bad ? -2 : 0;
+    else if (st >= 0) st |= min(lsp, 255) << 20;     // line-search passes (row_iters bits 20..27)
     return st;
+}
+
+// Per-line diagnostics (tvp_options_t.diag / iter_hist, include/tvprox.h): diag[0] lines,
+// diag[1] lines that ran the line search, diag[2] line-search passes, diag[3] stall
+// accepts; hist[b] lines that took b PN iterations (b = kHistBins - 1: not converged or
+// non-finite).  Integer atomics: the counts are deterministic.
+constexpr int kHistBins = 128;
+__device__ __forceinline__ void line_diag(int st, int32_t* diag, int32_t* hist) {
+    if (diag) {
+        atomicAdd(diag, 1);
+        const int lsn = st >= 0 ? (st >> 20) & 255 : 0;
+        if (lsn) {
+            atomicAdd(diag + 1, 1);
+            atomicAdd(diag + 2, lsn);
+        }
+        if (st >= 0 && ((st >> 16) & 1)) atomicAdd(diag + 3, 1);
+    }
+    if (hist) atomicAdd(hist + (st >= 0 ? min(st & 0xffff, kHistBins - 2) : kHistBins - 1), 1);
 }
 
 // ===========================================================================
@@ -255,7 +281,7 @@ template <typename T, int E> constexpr int col_minb() {
 #endif
 }
 
-template <typename T, int E, int LPR, bool PE, bool DYK, int WPB>
+template <typename T, int E, int LPR, bool PE, bool DYK, int WPB, bool LSP>
 __global__ void __launch_bounds__(WPB * 32, (row_minb<T, E>()))
 k_row_fwd(RowFwdArgs<T> a) {
     constexpr int G = 32 / LPR;
@@ -320,7 +346,7 @@ k_row_fwd(RowFwdArgs<T> a) {
             mask_window<E>(a.mask_in + r * a.mw, a.mw, l * E, wb, wp, wn);
         }
         const Comm<T, LPR, 1> C{l, 0, nullptr, nullptr};
-        int st = solve_line<T, E, LPR, 1, PE>(y, w, lam, n, valid, wp, wn, C, a.coarse != 0);
+        int st = solve_line<T, E, LPR, 1, PE, LSP>(y, w, lam, n, valid, wp, wn, C, a.coarse != 0, nullptr, a.ls_after);
         __syncwarp();
         if (valid) {
 #pragma unroll
@@ -375,6 +401,7 @@ k_row_fwd(RowFwdArgs<T> a) {
         if (valid && l == 0) {
             if (a.row_iters) a.row_iters[r] = st;
             if (a.iters_max) atomicMax(a.iters_max, st >= 0 ? (st & 0xffff) : (1 << 20));
+            line_diag(st, a.diag, a.hist);
         }
         __syncwarp();
     }
@@ -384,7 +411,7 @@ k_row_fwd(RowFwdArgs<T> a) {
 // Row forward with WPL warps per line (E samples per lane, 32*WPL lanes per line):
 // the block is one line at a time; cross-warp scans through shared memory.
 // ===========================================================================
-template <typename T, int E, int WPL, bool PE, bool DYK>
+template <typename T, int E, int WPL, bool PE, bool DYK, bool LSP>
 __global__ void __launch_bounds__(WPL * 32, (roww_minb<T, E, WPL>()))
 k_row_fwd_w(RowFwdArgs<T> a) {
     // Each line lane holds E contiguous samples loaded straight from HBM into
@@ -437,7 +464,8 @@ k_row_fwd_w(RowFwdArgs<T> a) {
             uint32_t wb;
             mask_window<E>(a.mask_in + r * a.mw, a.mw, i0, wb, wp, wn);
         }
-        const int st = solve_line<T, E, 32, WPL, PE>(y, w, lam, n, true, wp, wn, C, a.coarse != 0, coarse_v);
+        const int st = solve_line<T, E, 32, WPL, PE, LSP>(y, w, lam, n, true, wp, wn, C, a.coarse != 0, coarse_v,
+                                                          a.ls_after);
         st_contig<T, E>(a.dst0 + r * a.stride, i0, n, vec, w);
         if (DYK && a.dst1) {
             T p[E];
@@ -486,6 +514,7 @@ k_row_fwd_w(RowFwdArgs<T> a) {
         if (ll == 0) {
             if (a.row_iters) a.row_iters[r] = st;
             if (a.iters_max) atomicMax(a.iters_max, st >= 0 ? (st & 0xffff) : (1 << 20));
+            line_diag(st, a.diag, a.hist);
         }
     }
 }
@@ -537,7 +566,8 @@ __global__ void __launch_bounds__(WPB * 32) k_coarse_rows(RowFwdArgs<T> a) {
         const bool active = !__any_sync(FULL, bad) && lam > T(0) && nc >= 3;
         Lam<T, CPL, false> lc;
         lc.r = lam * (T(1) / T(EF));
-        pn_solve<T, CPL, 32, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active);
+        int lsp_;
+        pn_solve<T, CPL, 32, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active, kLsAfterDefault, lsp_);
         const T xn = shdn<32>(wc[0], 1);
         if (EF == 16) {
 #pragma unroll
@@ -633,7 +663,8 @@ __global__ void __launch_bounds__(WPB * 32) k_coarse_rows2(RowFwdArgs<T> a) {
         for (int q = 0; q < 4; ++q) pinc |= (4 * l + q >= nc - 1) ? (1u << q) : 0u;
         Lam<T, 4, false> lc;
         lc.r = lam * (T(1) / T(EF));
-        pn_solve<T, 4, 16, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active);
+        int lsp_;
+        pn_solve<T, 4, 16, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active, kLsAfterDefault, lsp_);
         const T xn = shdn<16>(wc[0], 1);
         if (rvalid) {
 #pragma unroll
@@ -650,7 +681,7 @@ __global__ void __launch_bounds__(WPB * 32) k_coarse_rows2(RowFwdArgs<T> a) {
 // ===========================================================================
 // Column forward: Dykstra column pass (tile of TC columns of one plane).
 // ===========================================================================
-template <typename T, int E, int LPR, int WPB>
+template <typename T, int E, int LPR, int WPB, bool LSP>
 __global__ void __launch_bounds__(WPB * 32, (col_minb<T, E>()))
 k_col_fwd(ColFwdArgs<T> a) {
     constexpr int G = 32 / LPR;
@@ -710,14 +741,18 @@ k_col_fwd(ColFwdArgs<T> a) {
                 mask_window<E>(a.mask_in + (p * W + c0 + c) * a.mw, a.mw, l * E, wb, wp, wn);
             }
             const Comm<T, LPR, 1> C{l, 0, nullptr, nullptr};
-            int st = solve_line<T, E, LPR, 1, false>(y, w, lam, H, valid, wp, wn, C, a.coarse != 0);
+            int st = solve_line<T, E, LPR, 1, false, LSP>(y, w, lam, H, valid, wp, wn, C, a.coarse != 0, nullptr,
+                                                          a.ls_after);
             if (valid) {
 #pragma unroll
                 for (int k = 0; k < E; ++k) {
                     int i = l * E + k;
                     if (i < H) bufX[c * LP + spad(i)] = w[k];
                 }
-                if (l == 0 && a.iters_max) atomicMax(a.iters_max, st >= 0 ? (st & 0xffff) : (1 << 20));
+                if (l == 0) {
+                    if (a.iters_max) atomicMax(a.iters_max, st >= 0 ? (st & 0xffff) : (1 << 20));
+                    line_diag(st, a.diag, a.hist);
+                }
             }
             if (a.mask_out) {
                 // column mask words from registers (as in k_row_fwd): each lane's <= 2
@@ -1050,9 +1085,12 @@ struct PlaneFwdArgs {
     uint32_t* saved;          // nullable (inference): K row-mask sets then K column-mask sets
     int mwr, mwc;
     int32_t* iters_max;       // nullable: 2K entries
+    int ls_after;             // PN iteration from which the projected line search runs (a-7)
+    int32_t* diag;            // nullable: accumulated line counters (line_diag)
+    int32_t* hist;            // nullable: [2K][kHistBins] (pass 2(k-1) rows, 2(k-1)+1 columns)
 };
 
-template <typename T, int ER, int EC, int WPB>
+template <typename T, int ER, int EC, int WPB, bool LSP>
 __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) : 1)) k_plane_fwd(PlaneFwdArgs<T> a) {
     constexpr int LPR = 8, G = 4;                     // 8 lanes per line, 4 lines per warp
     extern __shared__ __align__(16) unsigned char smraw_[];
@@ -1098,7 +1136,8 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
                 }
                 Lam<T, ER, false> lm;
                 lm.r = lamp;
-                const int st = solve_line<T, ER, LPR, 1, false>(y, w, lm, W, valid, wp0, wn0, Cm);
+                const int st = solve_line<T, ER, LPR, 1, false, LSP>(y, w, lm, W, valid, wp0, wn0, Cm, false, nullptr,
+                                                                     a.ls_after);
                 // codes of the lane's edges: next pass's warm bits and the saved mask
                 const T wnx = shdn<LPR>(w[0], 1);
                 uint32_t up, dn;
@@ -1117,7 +1156,10 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
                             ps[r * PW + i] = av[q] - w[q];
                         }
                     }
-                    if (l == 0 && a.iters_max) atomicMax(a.iters_max + 2 * (k - 1), st >= 0 ? (st & 0xffff) : (1 << 20));
+                    if (l == 0) {
+                        if (a.iters_max) atomicMax(a.iters_max + 2 * (k - 1), st >= 0 ? (st & 0xffff) : (1 << 20));
+                        line_diag(st, a.diag, a.hist ? a.hist + (2 * (k - 1)) * kHistBins : nullptr);
+                    }
                 }
                 if (a.saved) {
                     uint32_t* gw = mwb + grp * 8;
@@ -1148,7 +1190,8 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
                 }
                 Lam<T, EC, false> lm;
                 lm.r = lamp;
-                const int st = solve_line<T, EC, LPR, 1, false>(y, w, lm, H, valid, wp0, wn0, Cm);
+                const int st = solve_line<T, EC, LPR, 1, false, LSP>(y, w, lm, H, valid, wp0, wn0, Cm, false, nullptr,
+                                                                     a.ls_after);
                 const T wnx = shdn<LPR>(w[0], 1);
                 uint32_t up, dn;
                 const int e0 = l * EC, wlo = e0 >> 4;
@@ -1166,8 +1209,10 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
                             if (k < K) qs[h * PW + c] = bv[q] - w[q];
                         }
                     }
-                    if (l == 0 && a.iters_max)
-                        atomicMax(a.iters_max + 2 * (k - 1) + 1, st >= 0 ? (st & 0xffff) : (1 << 20));
+                    if (l == 0) {
+                        if (a.iters_max) atomicMax(a.iters_max + 2 * (k - 1) + 1, st >= 0 ? (st & 0xffff) : (1 << 20));
+                        line_diag(st, a.diag, a.hist ? a.hist + (2 * (k - 1) + 1) * kHistBins : nullptr);
+                    }
                 }
                 if (a.saved) {
                     uint32_t* gw = mwb + grp * 8;

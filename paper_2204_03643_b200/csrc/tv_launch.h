@@ -51,9 +51,26 @@ inline int lam_chunks(int64_t total, int64_t nout) {
     return (int)c;
 }
 
-template <typename T> cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s);
-template <typename T> cudaError_t launch_col_fwd(ColFwdArgs<T> a, cudaStream_t s);
-template <typename T> cudaError_t launch_plane_fwd(const PlaneFwdArgs<T>& a, cudaStream_t s);
+// Forward launchers per line-search flavour (LSP: parallel step search, f3) and the
+// dispatchers the C ABI calls (lsp = tvp_options_t.line_search == TVP_LS_PARALLEL).
+template <typename T> cudaError_t row_fwd_prepass(RowFwdArgs<T>& a, bool per_edge, bool dykstra, cudaStream_t s);
+template <typename T, bool LSP> cudaError_t launch_row_fwd_ls(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s);
+template <typename T, bool LSP> cudaError_t launch_col_fwd_ls(ColFwdArgs<T> a, cudaStream_t s);
+template <typename T, bool LSP> cudaError_t launch_plane_fwd_ls(const PlaneFwdArgs<T>& a, cudaStream_t s);
+template <typename T>
+inline cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s, bool lsp) {
+    cudaError_t e = row_fwd_prepass<T>(a, per_edge, dykstra, s);
+    if (e != cudaSuccess) return e;
+    return lsp ? launch_row_fwd_ls<T, true>(a, per_edge, dykstra, s) : launch_row_fwd_ls<T, false>(a, per_edge, dykstra, s);
+}
+template <typename T>
+inline cudaError_t launch_col_fwd(const ColFwdArgs<T>& a, cudaStream_t s, bool lsp) {
+    return lsp ? launch_col_fwd_ls<T, true>(a, s) : launch_col_fwd_ls<T, false>(a, s);
+}
+template <typename T>
+inline cudaError_t launch_plane_fwd(const PlaneFwdArgs<T>& a, cudaStream_t s, bool lsp) {
+    return lsp ? launch_plane_fwd_ls<T, true>(a, s) : launch_plane_fwd_ls<T, false>(a, s);
+}
 template <typename T> cudaError_t launch_plane_bwd(const PlaneBwdArgs<T>& a, cudaStream_t s);
 inline bool plane_fwd_supported(int64_t H, int64_t W) { return H > 32 && H <= 64 && W > 32 && W <= 64; }
 template <typename T> cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s);

@@ -10,32 +10,60 @@
 
 namespace tvp {
 
-// Persistent grid: min(work, SMs x resident blocks per SM) for this kernel.
+// Persistent grid: min(work, SMs x resident blocks per SM) for this kernel on the
+// current device.  The dynamic shared-memory opt-in and the occupancy query are per
+// (device, kernel, smem) -- the attribute belongs to the device context -- and cached
+// under a mutex; a failed opt-in (more shared memory than the device allows) is
+// returned as an error instead of launching.
+struct OccKey {
+    int dev;
+    const void* fn;
+    size_t smem;
+    bool operator==(const OccKey& o) const { return dev == o.dev && fn == o.fn && smem == o.smem; }
+};
+struct OccKeyHash {
+    size_t operator()(const OccKey& k) const {
+        return std::hash<const void*>()(k.fn) ^ (std::hash<size_t>()(k.smem) * 31u) ^ ((size_t)k.dev << 48);
+    }
+};
 template <typename K>
-static int persistent_grid(K kern, int threads, size_t smem, int64_t work_blocks) {
+static cudaError_t persistent_grid(K kern, int threads, size_t smem, int64_t work_blocks, int& grid) {
     static std::mutex mu;
-    static std::unordered_map<const void*, int> occ_cache;
+    static std::unordered_map<OccKey, int, OccKeyHash> occ_cache;
     int dev = 0;
-    cudaGetDevice(&dev);
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
     int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
     int occ = 0;
     {
         std::lock_guard<std::mutex> g(mu);
-        auto key = reinterpret_cast<const void*>(kern);
+        const OccKey key{dev, reinterpret_cast<const void*>(kern), smem};
         auto it = occ_cache.find(key);
         if (it == occ_cache.end()) {
-            if (smem > 48 * 1024)
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+            if (smem > 48 * 1024) {
+                e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+            }
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+            if (e != cudaSuccess) return e;
             occ_cache[key] = occ;
         } else {
             occ = it->second;
         }
     }
-    if (occ < 1) occ = 1;
+    if (occ < 1) return cudaErrorInvalidConfiguration;   // does not fit one SM
     int64_t g = std::min<int64_t>(work_blocks, (int64_t)sms * occ);
-    return (int)std::max<int64_t>(g, 1);
+    grid = (int)std::max<int64_t>(g, 1);
+    return cudaSuccess;
+}
+
+// Environment knobs of the A/B tuning builds: read once per process (thread-safe
+// function-local statics), never mutated afterwards.
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
 }
 
 #define TVP_GEO_DISPATCH(n, ...)                                               \
@@ -66,64 +94,61 @@ static int persistent_grid(K kern, int threads, size_t smem, int64_t work_blocks
 
 constexpr int kRowWPB = 4;
 
-// TVP_ROW_SPLIT selects the row-forward geometry for long lines (A/B measurements):
-// 0 = one warp per line, 2 = two warps per line (default), 4 = four warps per line.
+// TVP_ROW_SPLIT selects the row-forward geometry for 513..1024-sample lines (A/B
+// measurements): 0 = one warp per line (E = 32), 2 = two warps per line (default).
 static int row_fwd_split() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TVP_ROW_SPLIT");
-        v = e ? atoi(e) : 2;
-        if (v != 0 && v != 2 && v != 4) v = 2;
-    }
+    static const int v = env_int("TVP_ROW_SPLIT", 2) == 0 ? 0 : 2;
     return v;
 }
 // Warps per column-tile CTA (tile = WPB x 32 / LPR lines, x2 for one-warp lines), per
 // kernel and geometry from same-box A/B runs: fp32 one-warp
 // E = 16 column solves (C4) 4 warps, E = 14 column adjoints (C5) 4 warps, otherwise 8.
 // TVP_COL_WPB forces one value for every column kernel (A/B builds).
+// fp64 lines of E = 32 (513..1024 samples) use 4 warps (8 columns): 8 would need
+// 2 x 16 x 1055 x 8 B = 270 KB of shared memory, above the 227 KB per-CTA limit.
 template <typename T, int E, int LPR> constexpr int col_wpb_fwd() {
 #ifdef TVP_COL_WPB
     return TVP_COL_WPB;
 #else
-    return (sizeof(T) == 4 && E == 16 && LPR == 32) ? 4 : 8;
+    return ((sizeof(T) == 4 && E == 16 && LPR == 32) || (sizeof(T) == 8 && E == 32)) ? 4 : 8;
 #endif
 }
 template <typename T, int E, int LPR> constexpr int col_wpb_bwd() {
 #ifdef TVP_COL_WPB
     return TVP_COL_WPB;
 #else
-    return (sizeof(T) == 4 && E == 14) ? 4 : 8;
+    return ((sizeof(T) == 4 && E == 14) || (sizeof(T) == 8 && E == 32)) ? 4 : 8;
 #endif
 }
 
 // TVP_COARSE16=0 (A/B): half-warp lines (LPR = 16) solve cold without the coarse start.
 static bool coarse16_knob() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TVP_COARSE16");
-        v = e ? atoi(e) : 1;
-    }
-    return v != 0;
+    static const bool v = env_int("TVP_COARSE16", 1) != 0;
+    return v;
 }
 
-template <typename T, int E, int LPR, bool PE, bool DYK>
+template <typename T, int E, int LPR, bool PE, bool DYK, bool LSP>
 static cudaError_t row_fwd_t(RowFwdArgs<T> a, cudaStream_t s) {
     constexpr int G = 32 / LPR;
     if (LPR < 32 && !coarse16_knob()) a.coarse = 0;
     constexpr int LP = line_pitch<E, LPR>();
     const size_t smem = (size_t)kRowWPB * (DYK ? 2 : 1) * G * LP * sizeof(T) + (size_t)kRowWPB * 32 * 4;
-    auto kern = k_row_fwd<T, E, LPR, PE, DYK, kRowWPB>;
+    auto kern = k_row_fwd<T, E, LPR, PE, DYK, kRowWPB, LSP>;
     const int64_t groups = (a.nlines + G - 1) / G;
-    const int grid = persistent_grid(kern, kRowWPB * 32, smem, (groups + kRowWPB - 1) / kRowWPB);
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, kRowWPB * 32, smem, (groups + kRowWPB - 1) / kRowWPB, grid);
+    if (e != cudaSuccess) return e;
     kern<<<grid, kRowWPB * 32, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }
 
-template <typename T, int E, int WPL, bool PE, bool DYK>
+template <typename T, int E, int WPL, bool PE, bool DYK, bool LSP>
 static cudaError_t row_fwd_w_t(const RowFwdArgs<T>& a, cudaStream_t s) {
-    auto kern = k_row_fwd_w<T, E, WPL, PE, DYK>;
-    const int grid = persistent_grid(kern, WPL * 32, 0, a.nlines);
+    auto kern = k_row_fwd_w<T, E, WPL, PE, DYK, LSP>;
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, WPL * 32, 0, a.nlines, grid);
+    if (e != cudaSuccess) return e;
     kern<<<grid, WPL * 32, 0, s>>>(a);
     count_launch();
     return cudaGetLastError();
@@ -131,12 +156,8 @@ static cudaError_t row_fwd_w_t(const RowFwdArgs<T>& a, cudaStream_t s) {
 
 // TVP_COARSE=0 disables the coarse initial bound set of cold solves (A/B only).
 static bool coarse_knob() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TVP_COARSE");
-        v = (e && atoi(e) == 0) ? 0 : 1;
-    }
-    return v != 0;
+    static const bool v = env_int("TVP_COARSE", 1) != 0;
+    return v;
 }
 
 // Coarse pre-pass for the long-row geometry (E = 16 fine blocks): writes the initial
@@ -145,7 +166,9 @@ template <typename T, int EF, int CPL, bool DYK>
 static cudaError_t coarse_rows_t(const RowFwdArgs<T>& a, cudaStream_t s) {
     constexpr int WPB = 4;
     auto kern = k_coarse_rows<T, EF, CPL, DYK, WPB>;
-    const int grid = persistent_grid(kern, WPB * 32, 0, (a.nlines + WPB - 1) / WPB);
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, WPB * 32, 0, (a.nlines + WPB - 1) / WPB, grid);
+    if (e != cudaSuccess) return e;
     kern<<<grid, WPB * 32, 0, s>>>(a);
     count_launch();
     return cudaGetLastError();
@@ -156,86 +179,80 @@ static cudaError_t coarse_rows2_t(const RowFwdArgs<T>& a, cudaStream_t s) {
     constexpr int WPB = 4;
     auto kern = k_coarse_rows2<T, DYK, WPB>;
     const int64_t pairs = (a.nlines + 1) / 2;
-    const int grid = persistent_grid(kern, WPB * 32, 0, (pairs + WPB - 1) / WPB);
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, WPB * 32, 0, (pairs + WPB - 1) / WPB, grid);
+    if (e != cudaSuccess) return e;
     kern<<<grid, WPB * 32, 0, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }
 
-// TVP_COARSE_PASS=0 keeps the coarse solve inside the long-row forward kernel (A/B);
-// TVP_COARSE_PASS=1 one line per warp, 2 (default) two lines per warp.
+// TVP_COARSE_PASS=0 keeps the coarse solve inside the fine forward kernel (A/B); the
+// default runs it as a pre-pass (two lines per warp for 513..1024-sample lines).
 static int coarse_pass_knob() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TVP_COARSE_PASS");
-        v = e ? atoi(e) : 2;
-    }
+    static const int v = env_int("TVP_COARSE_PASS", 2);
     return v;
 }
 
+// Row-forward set-up shared by both line-search flavours: the coarse initial bound set
+// of cold solves (reading O7) -- in-kernel (a.coarse = 1) or, for the E = 16 fine
+// geometries, as a separate pre-pass kernel that writes the initial mask into
+// mask_out, which the fine kernel then reads as its warm start (a.mask_in).
 template <typename T>
-cudaError_t launch_row_fwd(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s) {
-    cudaError_t e = cudaSuccess;
+cudaError_t row_fwd_prepass(RowFwdArgs<T>& a, bool per_edge, bool dykstra, cudaStream_t s) {
     a.coarse = (a.mask_in == nullptr && !per_edge && coarse_knob()) ? 1 : 0;
-    const int split = row_fwd_split();
+    if (a.n > 1024) {
+        if (TVP_COARSE_MAXWPL < 4) a.coarse = 0;   // long rows: in-kernel coarse solve
+        return cudaSuccess;
+    }
+    if (!(a.coarse && a.mask_out && a.n >= 3 * 4 && coarse_pass_knob())) return cudaSuccess;
+    cudaError_t e = cudaSuccess;
+    if (a.n > 512 && row_fwd_split() == 2) {
+        e = dykstra ? coarse_rows2_t<T, true>(a, s) : coarse_rows2_t<T, false>(a, s);
+    } else if (a.n > 256 && a.n <= 512 && pick_geo(a.n).E == 16) {
+        // (E <= 8 geometries keep the in-kernel coarse solve: their short loops do not
+        // spill the I-cache, and a separate pass measured slower at C5)
+        e = dykstra ? coarse_rows_t<T, 16, 1, true>(a, s) : coarse_rows_t<T, 16, 1, false>(a, s);
+    } else {
+        return cudaSuccess;
+    }
+    if (e != cudaSuccess) return e;
+    a.mask_in = a.mask_out;                      // in place: each line reads its words before writing them
+    a.coarse = 0;
+    return cudaSuccess;
+}
+
+template <typename T, bool LSP>
+cudaError_t launch_row_fwd_ls(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
     if (a.n > 1024) {
         // long 1D rows (f4): one CTA of WPL warps holds the row in registers, E = 16
-        // (fp32) / 8 (fp64) samples per lane; in-kernel coarse solve if TVP_COARSE_MAXWPL >= WPL
-        if (TVP_COARSE_MAXWPL < 4) a.coarse = 0;
+        // (fp32) / 8 (fp64) samples per lane; in-kernel coarse solve
         if constexpr (sizeof(T) == 4) {
-            if (a.n <= 2048) return per_edge ? row_fwd_w_t<T, 16, 4, true, false>(a, s) : row_fwd_w_t<T, 16, 4, false, false>(a, s);
-            if (a.n <= 4096) return per_edge ? row_fwd_w_t<T, 16, 8, true, false>(a, s) : row_fwd_w_t<T, 16, 8, false, false>(a, s);
-            return per_edge ? row_fwd_w_t<T, 16, 16, true, false>(a, s) : row_fwd_w_t<T, 16, 16, false, false>(a, s);
+            if (a.n <= 2048) return per_edge ? row_fwd_w_t<T, 16, 4, true, false, LSP>(a, s) : row_fwd_w_t<T, 16, 4, false, false, LSP>(a, s);
+            if (a.n <= 4096) return per_edge ? row_fwd_w_t<T, 16, 8, true, false, LSP>(a, s) : row_fwd_w_t<T, 16, 8, false, false, LSP>(a, s);
+            return per_edge ? row_fwd_w_t<T, 16, 16, true, false, LSP>(a, s) : row_fwd_w_t<T, 16, 16, false, false, LSP>(a, s);
         } else {
-            if (a.n <= 2048) return per_edge ? row_fwd_w_t<T, 8, 8, true, false>(a, s) : row_fwd_w_t<T, 8, 8, false, false>(a, s);
-            return per_edge ? row_fwd_w_t<T, 8, 16, true, false>(a, s) : row_fwd_w_t<T, 8, 16, false, false>(a, s);
+            if (a.n <= 2048) return per_edge ? row_fwd_w_t<T, 8, 8, true, false, LSP>(a, s) : row_fwd_w_t<T, 8, 8, false, false, LSP>(a, s);
+            return per_edge ? row_fwd_w_t<T, 8, 16, true, false, LSP>(a, s) : row_fwd_w_t<T, 8, 16, false, false, LSP>(a, s);
         }
     }
-    if (a.coarse && a.mask_out && a.n >= 3 * 4 && coarse_pass_knob()) {
-        // coarse pre-pass with the block size of the fine geometry (E samples per lane)
-        if (a.n > 512 && split == 2) {
-            if (coarse_pass_knob() == 2)
-                e = dykstra ? coarse_rows2_t<T, true>(a, s) : coarse_rows2_t<T, false>(a, s);
-            else
-                e = dykstra ? coarse_rows_t<T, 16, 2, true>(a, s) : coarse_rows_t<T, 16, 2, false>(a, s);
-        } else if (a.n > 256 && a.n <= 512 && pick_geo(a.n).E == 16) {
-            // (E <= 8 geometries keep the in-kernel coarse solve: their short loops do
-            // not spill the I-cache, and a separate pass measured slower at C5)
-            e = dykstra ? coarse_rows_t<T, 16, 1, true>(a, s) : coarse_rows_t<T, 16, 1, false>(a, s);
-        } else {
-            goto no_pass;
-        }
-        if (e != cudaSuccess) return e;
-        a.mask_in = a.mask_out;                  // in place: each line reads its words before writing them
-        a.coarse = 0;
-    }
-no_pass:
-    if (a.n > 512 && split == 2) {               // 1024-sample lines: two warps x 16 samples per lane
-        if (dykstra) return row_fwd_w_t<T, 16, 2, false, true>(a, s);
-        if (per_edge) return row_fwd_w_t<T, 16, 2, true, false>(a, s);
-        return row_fwd_w_t<T, 16, 2, false, false>(a, s);
-    }
-    if (a.n > 512 && split == 4) {               // four warps x 8 samples per lane
-        if (dykstra) return row_fwd_w_t<T, 8, 4, false, true>(a, s);
-        if (per_edge) return row_fwd_w_t<T, 8, 4, true, false>(a, s);
-        return row_fwd_w_t<T, 8, 4, false, false>(a, s);
-    }
-    if (a.n > 256 && a.n <= 512 && split == 4) { // 512-sample lines: two warps x 8
-        if (dykstra) return row_fwd_w_t<T, 8, 2, false, true>(a, s);
-        if (per_edge) return row_fwd_w_t<T, 8, 2, true, false>(a, s);
-        return row_fwd_w_t<T, 8, 2, false, false>(a, s);
+    if (a.n > 512 && row_fwd_split() == 2) {     // 1024-sample lines: two warps x 16 samples per lane
+        if (dykstra) return row_fwd_w_t<T, 16, 2, false, true, LSP>(a, s);
+        if (per_edge) return row_fwd_w_t<T, 16, 2, true, false, LSP>(a, s);
+        return row_fwd_w_t<T, 16, 2, false, false, LSP>(a, s);
     }
     TVP_GEO_DISPATCH(a.n, {
-        if (dykstra) e = row_fwd_t<T, E_, L_, false, true>(a, s);
-        else if (per_edge) e = row_fwd_t<T, E_, L_, true, false>(a, s);
-        else e = row_fwd_t<T, E_, L_, false, false>(a, s);
+        if (dykstra) e = row_fwd_t<T, E_, L_, false, true, LSP>(a, s);
+        else if (per_edge) e = row_fwd_t<T, E_, L_, true, false, LSP>(a, s);
+        else e = row_fwd_t<T, E_, L_, false, false, LSP>(a, s);
     });
     return e;
 }
 
 template <int WPB, int LPR> constexpr int col_tile() { return WPB * (32 / LPR) * (LPR == 32 ? 2 : 1); }
 
-template <typename T, int E, int LPR>
+template <typename T, int E, int LPR, bool LSP>
 static cudaError_t col_fwd_t(ColFwdArgs<T> a, cudaStream_t s) {
     constexpr int WPB = col_wpb_fwd<T, E, LPR>();
     constexpr int LP = line_pitch<E, LPR>();
@@ -243,19 +260,21 @@ static cudaError_t col_fwd_t(ColFwdArgs<T> a, cudaStream_t s) {
     a.TC = TC;
     if (LPR < 32 && !coarse16_knob()) a.coarse = 0;
     const size_t smem = (size_t)2 * TC * LP * sizeof(T) + (size_t)WPB * 64 * 4;
-    auto kern = k_col_fwd<T, E, LPR, WPB>;
+    auto kern = k_col_fwd<T, E, LPR, WPB, LSP>;
     const int64_t tiles = a.planes * ((a.W + TC - 1) / TC);
-    const int grid = persistent_grid(kern, WPB * 32, smem, tiles);
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, WPB * 32, smem, tiles, grid);
+    if (e != cudaSuccess) return e;
     kern<<<grid, WPB * 32, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_col_fwd(ColFwdArgs<T> a, cudaStream_t s) {
+template <typename T, bool LSP>
+cudaError_t launch_col_fwd_ls(ColFwdArgs<T> a, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
     a.coarse = (a.mask_in == nullptr && coarse_knob()) ? 1 : 0;
-    TVP_GEO_DISPATCH(a.H, { e = col_fwd_t<T, E_, L_>(a, s); });
+    TVP_GEO_DISPATCH(a.H, { e = col_fwd_t<T, E_, L_, LSP>(a, s); });
     return e;
 }
 
@@ -266,7 +285,9 @@ static cudaError_t row_bwd_t(const RowBwdArgs<T>& a, cudaStream_t s) {
     const size_t smem = (size_t)kRowWPB * (DYK ? 2 : 1) * G * LP * sizeof(T);
     auto kern = k_row_bwd<T, E, LPR, DYK, PE, kRowWPB>;
     const int64_t groups = (a.nlines + G - 1) / G;
-    const int grid = persistent_grid(kern, kRowWPB * 32, smem, (groups + kRowWPB - 1) / kRowWPB);
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, kRowWPB * 32, smem, (groups + kRowWPB - 1) / kRowWPB, grid);
+    if (e != cudaSuccess) return e;
     kern<<<grid, kRowWPB * 32, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
@@ -275,7 +296,9 @@ static cudaError_t row_bwd_t(const RowBwdArgs<T>& a, cudaStream_t s) {
 template <typename T, int E, int WPL, bool DYK, bool PE>
 static cudaError_t row_bwd_w_t(const RowBwdArgs<T>& a, cudaStream_t s) {
     auto kern = k_row_bwd_w<T, E, WPL, DYK, PE>;
-    const int grid = persistent_grid(kern, WPL * 32, 0, a.nlines);
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, WPL * 32, 0, a.nlines, grid);
+    if (e != cudaSuccess) return e;
     kern<<<grid, WPL * 32, 0, s>>>(a);
     count_launch();
     return cudaGetLastError();
@@ -284,8 +307,6 @@ static cudaError_t row_bwd_w_t(const RowBwdArgs<T>& a, cudaStream_t s) {
 template <typename T>
 cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
-    // TVP_BWD_SPLIT (A/B): warps per long line; default 2 x 16 samples (measured best for n = 1024)
-    static const int bsplit = getenv("TVP_BWD_SPLIT") ? atoi(getenv("TVP_BWD_SPLIT")) : 2;
     if (a.n > 1024) {                             // long 1D rows (f4): one CTA of WPL warps per row
         if constexpr (sizeof(T) == 4) {
             if (a.n <= 2048) return per_edge ? row_bwd_w_t<T, 16, 4, false, true>(a, s) : row_bwd_w_t<T, 16, 4, false, false>(a, s);
@@ -296,20 +317,10 @@ cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, 
             return per_edge ? row_bwd_w_t<T, 8, 16, false, true>(a, s) : row_bwd_w_t<T, 8, 16, false, false>(a, s);
         }
     }
-    if (a.n > 512 && bsplit == 1) {               // A/B: 1 warp x 32 samples per thread
-        if (dykstra) return row_bwd_w_t<T, 32, 1, true, false>(a, s);
-        if (per_edge) return row_bwd_w_t<T, 32, 1, false, true>(a, s);
-        return row_bwd_w_t<T, 32, 1, false, false>(a, s);
-    }
-    if (a.n > 512 && bsplit == 2) {               // A/B: 2 warps x 16 samples per thread
+    if (a.n > 512) {                              // 2 warps x 16 samples per thread (same-box A/B best)
         if (dykstra) return row_bwd_w_t<T, 16, 2, true, false>(a, s);
         if (per_edge) return row_bwd_w_t<T, 16, 2, false, true>(a, s);
         return row_bwd_w_t<T, 16, 2, false, false>(a, s);
-    }
-    if (a.n > 512) {                              // long lines: 4 warps x 8 samples per thread
-        if (dykstra) return row_bwd_w_t<T, 8, 4, true, false>(a, s);
-        if (per_edge) return row_bwd_w_t<T, 8, 4, false, true>(a, s);
-        return row_bwd_w_t<T, 8, 4, false, false>(a, s);
     }
     if (a.n > 256) {                              // 2 warps x 8
         if (dykstra) return row_bwd_w_t<T, 8, 2, true, false>(a, s);
@@ -333,7 +344,9 @@ static cudaError_t col_bwd_t(ColBwdArgs<T> a, cudaStream_t s) {
     const size_t smem = (size_t)2 * TC * LP * sizeof(T);
     auto kern = k_col_bwd<T, E, LPR, WPB>;
     const int64_t tiles = a.planes * ((a.W + TC - 1) / TC);
-    const int grid = persistent_grid(kern, WPB * 32, smem, tiles);
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, WPB * 32, smem, tiles, grid);
+    if (e != cudaSuccess) return e;
     kern<<<grid, WPB * 32, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
@@ -382,33 +395,27 @@ cudaError_t launch_axpby(const T* x, T* y, T a, T b, int64_t n, cudaStream_t s) 
 #ifndef TVP_PLANE_WPB
 #define TVP_PLANE_WPB 8
 #endif
-template <typename T, int ER, int EC>
+template <typename T, int ER, int EC, bool LSP>
 static cudaError_t plane_fwd_t(const PlaneFwdArgs<T>& a, cudaStream_t s) {
     constexpr int WPB = TVP_PLANE_WPB;
     const int PW = a.W | 1;
     const size_t smem = (size_t)3 * a.H * PW * sizeof(T) + (size_t)WPB * 32 * 4 + (size_t)4 * 16 * 32 * 4;
-    auto kern = k_plane_fwd<T, ER, EC, WPB>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    int dev = 0, sms = 148, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WPB * 32, smem);
-    const int64_t g = std::min<int64_t>(a.planes, (int64_t)sms * std::max(occ, 1));
-    kern<<<(int)std::max<int64_t>(g, 1), WPB * 32, smem, s>>>(a);
+    auto kern = k_plane_fwd<T, ER, EC, WPB, LSP>;
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, WPB * 32, smem, a.planes, grid);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, WPB * 32, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_plane_fwd(const PlaneFwdArgs<T>& a, cudaStream_t s) {
+template <typename T, bool LSP>
+cudaError_t launch_plane_fwd_ls(const PlaneFwdArgs<T>& a, cudaStream_t s) {
     const int er = pick_geo(a.W).E, ec = pick_geo(a.H).E;
-    if (er == 7 && ec == 7) return plane_fwd_t<T, 7, 7>(a, s);
-    if (er == 7) return plane_fwd_t<T, 7, 8>(a, s);
-    if (ec == 7) return plane_fwd_t<T, 8, 7>(a, s);
-    return plane_fwd_t<T, 8, 8>(a, s);
+    if (er == 7 && ec == 7) return plane_fwd_t<T, 7, 7, LSP>(a, s);
+    if (er == 7) return plane_fwd_t<T, 7, 8, LSP>(a, s);
+    if (ec == 7) return plane_fwd_t<T, 8, 7, LSP>(a, s);
+    return plane_fwd_t<T, 8, 8, LSP>(a, s);
 }
 
 template <typename T, int ER, int EC>
@@ -417,16 +424,10 @@ static cudaError_t plane_bwd_t(const PlaneBwdArgs<T>& a, cudaStream_t s) {
     const int PW = a.W | 1;
     const size_t smem = (size_t)2 * a.H * PW * sizeof(T);
     auto kern = k_plane_bwd<T, ER, EC, WPB>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    int dev = 0, sms = 148, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WPB * 32, smem);
-    const int64_t g = std::min<int64_t>(a.planes, (int64_t)sms * std::max(occ, 1));
-    kern<<<(int)std::max<int64_t>(g, 1), WPB * 32, smem, s>>>(a);
+    int grid = 0;
+    cudaError_t e = persistent_grid(kern, WPB * 32, smem, a.planes, grid);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, WPB * 32, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
 }
@@ -440,14 +441,17 @@ cudaError_t launch_plane_bwd(const PlaneBwdArgs<T>& a, cudaStream_t s) {
     return plane_bwd_t<T, 8, 8>(a, s);
 }
 
-#define TVP_INSTANTIATE(T)                                                                         \
-    template cudaError_t launch_plane_fwd<T>(const PlaneFwdArgs<T>&, cudaStream_t);                \
+// Explicit instantiations, split over several translation units (tv_inst_*.cu) so the
+// build compiles them in parallel.
+#define TVP_INST_ROWFWD(T, LSP) template cudaError_t launch_row_fwd_ls<T, LSP>(RowFwdArgs<T>, bool, bool, cudaStream_t);
+#define TVP_INST_COLFWD(T, LSP) template cudaError_t launch_col_fwd_ls<T, LSP>(ColFwdArgs<T>, cudaStream_t);
+#define TVP_INST_PLANE(T, LSP) template cudaError_t launch_plane_fwd_ls<T, LSP>(const PlaneFwdArgs<T>&, cudaStream_t);
+#define TVP_INST_BWD(T)                                                                            \
+    template cudaError_t row_fwd_prepass<T>(RowFwdArgs<T>&, bool, bool, cudaStream_t);             \
     template cudaError_t launch_plane_bwd<T>(const PlaneBwdArgs<T>&, cudaStream_t);                \
-    template cudaError_t launch_row_fwd<T>(RowFwdArgs<T>, bool, bool, cudaStream_t);        \
-    template cudaError_t launch_col_fwd<T>(ColFwdArgs<T>, cudaStream_t);                           \
     template cudaError_t launch_row_bwd<T>(const RowBwdArgs<T>&, bool, bool, cudaStream_t);        \
     template cudaError_t launch_col_bwd<T>(ColBwdArgs<T>, cudaStream_t);                           \
-    template cudaError_t launch_lam_reduce<T>(const LamReduceArgs<T>&, cudaStream_t);                \
+    template cudaError_t launch_lam_reduce<T>(const LamReduceArgs<T>&, cudaStream_t);              \
     template cudaError_t launch_softplus<T>(const T*, T*, const T*, T*, int64_t, bool, cudaStream_t);\
     template cudaError_t launch_axpby<T>(const T*, T*, T, T, int64_t, cudaStream_t);
 

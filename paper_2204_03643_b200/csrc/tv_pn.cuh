@@ -241,19 +241,16 @@ __device__ __forceinline__ int prev_bit(uint32_t m, int k) {
     return 31 - __clz(mm);
 }
 
-// Iterations after which a line switches from projected full Newton steps to the
-// projected Armijo line search (DESIGN.md a-7).
-#ifndef TVP_LS_AFTER
-#define TVP_LS_AFTER 12
-#endif
-constexpr int kLsAfter = TVP_LS_AFTER;
-// f3: TVP_LS_PARALLEL=1 replaces the sequential backtracking by a parallel
-// step search -- four step sizes alpha, alpha/2, alpha/4, alpha/8 evaluated in one
-// fused pass with one reduction, the largest Armijo-accepted one taken (P:188 compares
-// the two; measured in DESIGN.md section 10).
-#ifndef TVP_LS_PARALLEL
-#define TVP_LS_PARALLEL 0
-#endif
+// Line-search configuration (DESIGN.md a-7, f3).  From PN iteration ls_after on (a runtime
+// argument, tvp_options_t.ls_after; default kLsAfterDefault), a step whose full Newton
+// point leaves the box is globalised by the projected Armijo line search of P:188;
+// before that it is the projected full step.  The search flavour is a template
+// parameter LSP of the solver (separate kernel instantiations, so the default kernels
+// carry no code of the other flavour): false = sequential quadratic-interpolation
+// backtracking ("only iterates a few times"), true = the parallel step search
+// (SURVEY 8(f) f3): four step sizes alpha, alpha/2, alpha/4, alpha/8 evaluated in one
+// fused pass with one reduction, the largest Armijo-accepted one taken.
+constexpr int kLsAfterDefault = 12;
 
 template <typename T> __device__ __forceinline__ T big_();
 template <> __device__ __forceinline__ float big_<float>() { return 3.0e38f; }
@@ -266,11 +263,11 @@ template <> __device__ __forceinline__ double big_<double>() { return 1.0e300; }
 // of the line (slack bound).  Returns the line status: iterations (| 1<<16 if
 // accepted at a stall), or -1 (max iterations, w = x(u)).
 // ---------------------------------------------------------------------------
-template <typename T, int E, int LPR, int WPL, bool PE>
+template <typename T, int E, int LPR, int WPL, bool PE, bool LSP = false>
 __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], uint32_t pin,
                                         uint32_t warm_pos, uint32_t warm_neg,
                                         const Lam<T, E, PE>& lam, const Comm<T, LPR, WPL>& C,
-                                        bool active) {
+                                        bool active, int ls_after, int& ls_passes) {
     warm_pos &= ~pin;
     warm_neg &= ~pin;
 #pragma unroll
@@ -289,6 +286,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
     bool run = active, first = true, fin = false, uchg = true, fin_direct = false;
     bool conv = false, stall = false;
     int it = 0;
+    ls_passes = 0;
     for (int itw = 0;; ++itw) {
         // ---------------- P1: bound set at u (Bertsekas rule: at a bound with the
         // gradient g = D x(u) pointing out of the box) fused with the lane-local part
@@ -387,7 +385,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         T A = fabs(ub) + at;
         C.template scan_fwd2<4>(sg, r, A);
         const T xnext = C.template next<5>(w[0]);
-        const bool lsmode = C.uany(run && !first && (it + 1 >= kLsAfter));
+        const bool lsmode = C.uany(run && !first && (it + 1 >= ls_after));
         bool ok = true, clip = false, chg = false;
         if (!lsmode) {
             // The tests accumulate non-negative violations on the FMA pipe instead of
@@ -463,7 +461,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
 
         // ---------------- step (LS mode): full Newton step when it stays in the box,
         // else the projected Armijo line search with quadratic-interpolation
-        // backtracking of P:188 -- the globalisation safeguard after kLsAfter iterations.
+        // backtracking of P:188 -- the globalisation safeguard from iteration ls_after on.
         const bool fast = lsmode && run && (first || !clip);
         if (!lsmode) {
             uchg = chg || first;
@@ -476,7 +474,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             uchg = chg || first;
         }
         bool pending = lsmode && run && !fast;
-        if (TVP_LS_PARALLEL && C.uany(pending)) {
+        if (LSP && C.uany(pending)) {
             constexpr int NA = 4;
             T abase = T(1), alpha = T(0);
             bool accepted = false, lchg = false;
@@ -525,6 +523,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
 #pragma unroll
                 for (int j = 0; j < NA; ++j) chj[j] = C.any(ch[j]);
                 if (pending) {
+                    ++ls_passes;
 #pragma unroll
                     for (int j = NA - 1; j >= 0; --j) {     // keep the largest accepted alpha
                         const T gain = T(-0.5) * F[j];
@@ -588,6 +587,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                 if (pending && C.first_lane()) printf("[tvp]   LS trial %d alpha %g F %g G %g S %g ch %d\n", trial, (double)alpha, (double)F, (double)G, (double)S, (int)ch);
 #endif
                 if (pending) {
+                    ++ls_passes;
                     const T gain = T(-0.5) * F;          // phi(u(alpha)) - phi(u)
                     if (gain >= T(1e-4) * G) {
                         // an accepted step without measurable ascent is a rounding-level
@@ -664,7 +664,8 @@ __device__ __forceinline__ void coarse_init(const T (&y)[E], T lam_r, int n, boo
         T yc[WPL], uc[WPL], wc[WPL];
         yc[0] = ybar;
         const uint32_t pinc = (ll >= nc - 1) ? 1u : 0u;
-        pn_solve<T, WPL, LPR, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active);
+        int lsp_;
+        pn_solve<T, WPL, LPR, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active, kLsAfterDefault, lsp_);
         const T xn = shdn<LPR>(wc[0], 1);
         if (ll < nc - 1) {
             cpos = xn > wc[0] ? top : 0u;
@@ -682,7 +683,8 @@ __device__ __forceinline__ void coarse_init(const T (&y)[E], T lam_r, int n, boo
             pinc |= (l * WPL + q >= nc - 1) ? (1u << q) : 0u;
         }
         const Comm<T, 32, 1> Cw{l, 0, nullptr, nullptr};
-        pn_solve<T, WPL, 32, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, Cw, active);
+        int lsp_;
+        pn_solve<T, WPL, 32, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, Cw, active, kLsAfterDefault, lsp_);
         const T xn = shdn<32>(wc[0], 1);
         const int cl = ll / WPL, cq = ll % WPL;
 #pragma unroll

@@ -16,18 +16,21 @@ namespace tvp {
 static thread_local std::string g_err;
 static thread_local int64_t g_launches = 0;
 void count_launch() { ++g_launches; }
-// f2 fused on-chip 2D path switch (default on; TVP_FUSED2D=0 or tvp_set_fused2d(0) -> staged)
-static bool fused2d_default() {
-    const char* e = getenv("TVP_FUSED2D");
-    return !(e && atoi(e) == 0);
+// f2 fused on-chip 2D path: the calling thread's default for tvp_options_t.fused2d = -1
+// (initially on; TVP_FUSED2D=0 in the environment -> staged).
+static bool fused2d_env() {
+    static const bool v = [] {
+        const char* e = getenv("TVP_FUSED2D");
+        return !(e && atoi(e) == 0);
+    }();
+    return v;
 }
-static bool g_fused2d = fused2d_default();
+static thread_local int g_fused2d = -1;     // -1: not set on this thread (environment default)
 int geo16_knob() {
-    static int v = -1;
-    if (v < 0) {
+    static const int v = [] {
         const char* e = getenv("TVP_GEO16");
-        v = e ? atoi(e) : TVP_GEO16_DEFAULT;
-    }
+        return e ? atoi(e) : TVP_GEO16_DEFAULT;
+    }();
     return v;
 }
 }  // namespace tvp
@@ -44,6 +47,27 @@ static tvp_status_t cuda_status(cudaError_t e, const char* where) {
     return TVP_ECUDA;
 }
 static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// Resolved per-call options (tvp_options_t, include/tvprox.h).
+struct Opts {
+    bool fused2d;
+    bool lsp;
+    int ls_after;
+    int32_t* diag;
+    int32_t* hist;
+};
+static bool resolve_opts(const tvp_options_t* o, Opts& r) {
+    const int f = o ? o->fused2d : -1;
+    const int ls = o ? o->line_search : TVP_LS_BACKTRACK;
+    const int after = o ? o->ls_after : 0;
+    if (f < -1 || f > 1 || (ls != TVP_LS_BACKTRACK && ls != TVP_LS_PARALLEL) || after < 0) return false;
+    r.fused2d = f == -1 ? (g_fused2d == -1 ? fused2d_env() : g_fused2d != 0) : f != 0;
+    r.lsp = ls == TVP_LS_PARALLEL;
+    r.ls_after = after == 0 ? kLsAfterDefault : after;
+    r.diag = o ? o->diag : nullptr;
+    r.hist = o ? o->iter_hist : nullptr;
+    return true;
+}
 static int64_t mask_words(int64_t n) { return n <= 1 ? 0 : (n - 1 + 15) / 16; }
 
 extern "C" {
@@ -66,9 +90,17 @@ const char* tvp_status_string(tvp_status_t s) {
 }
 int64_t tvp_max_line(tvp_dtype_t dt) { (void)dt; return kMaxLine; }
 int tvp_set_fused2d(int enable) {
-    const int prev = g_fused2d ? 1 : 0;
-    g_fused2d = enable != 0;
+    const int prev = g_fused2d == -1 ? (fused2d_env() ? 1 : 0) : g_fused2d;
+    g_fused2d = enable != 0 ? 1 : 0;
     return prev;
+}
+void tvp_options_default(tvp_options_t* o) {
+    if (!o) return;
+    o->fused2d = -1;
+    o->line_search = TVP_LS_BACKTRACK;
+    o->ls_after = 0;
+    o->diag = nullptr;
+    o->iter_hist = nullptr;
 }
 int64_t tvp_max_line_1d(tvp_dtype_t dt) { return dt == TVP_F64 ? kMaxLine1DF64 : kMaxLine1DF32; }
 size_t tv1d_mask_words(int64_t n) { return (size_t)mask_words(n); }
@@ -115,7 +147,7 @@ size_t tv2d_workspace_bytes(tvp_dtype_t dt, int64_t N, int64_t C, int64_t H, int
 template <typename T>
 static tvp_status_t tv1d_fwd_impl(const void* y, void* x, int64_t batch, int64_t n, int64_t stride,
                                   const void* lam, tvp_lam_mode_t lm, double lam_scalar, uint32_t* mask,
-                                  int32_t* row_iters, cudaStream_t s, const uint32_t* mask_in = nullptr) {
+                                  int32_t* row_iters, cudaStream_t s, const uint32_t* mask_in, const Opts& o) {
     RowFwdArgs<T> a{};
     a.src0 = static_cast<const T*>(y);
     a.src1 = nullptr;
@@ -134,12 +166,18 @@ static tvp_status_t tv1d_fwd_impl(const void* y, void* x, int64_t batch, int64_t
     a.mw = (int)mask_words(n);
     a.row_iters = row_iters;
     a.iters_max = nullptr;
-    return cuda_status(launch_row_fwd<T>(a, lm == TVP_LAM_PER_EDGE, false, s), "tv1d_prox_fwd");
+    a.ls_after = o.ls_after;
+    a.diag = o.diag;
+    a.hist = o.hist;
+    return cuda_status(launch_row_fwd<T>(a, lm == TVP_LAM_PER_EDGE, false, s, o.lsp), "tv1d_prox_fwd");
 }
 
-extern "C" tvp_status_t tv1d_prox_fwd(tvp_dtype_t dt, const void* y, void* x, int64_t batch, int64_t n,
-                                      int64_t stride, const void* lam, tvp_lam_mode_t lm, double lam_scalar,
-                                      uint32_t* mask, int32_t* row_iters, tvp_stream_t stream) {
+extern "C" tvp_status_t tv1d_prox_fwd_ex(tvp_dtype_t dt, const void* y, void* x, int64_t batch, int64_t n,
+                                         int64_t stride, const void* lam, tvp_lam_mode_t lm, double lam_scalar,
+                                         const uint32_t* mask_in, uint32_t* mask_out, int32_t* row_iters,
+                                         const tvp_options_t* opts, tvp_stream_t stream) {
+    Opts o;
+    if (!resolve_opts(opts, o)) return fail(TVP_EINVAL, "tv1d_prox_fwd: invalid tvp_options_t");
     if (dt != TVP_F32 && dt != TVP_F64) return fail(TVP_EINVAL, "tv1d_prox_fwd: bad dtype");
     if (batch < 0 || n < 1 || stride < n) return fail(TVP_EINVAL, "tv1d_prox_fwd: need batch >= 0, n >= 1, stride >= n");
     if (lm != TVP_LAM_SCALAR && lm != TVP_LAM_PER_ROW && lm != TVP_LAM_PER_EDGE)
@@ -151,8 +189,16 @@ extern "C" tvp_status_t tv1d_prox_fwd(tvp_dtype_t dt, const void* y, void* x, in
     if (lm != TVP_LAM_SCALAR && !lam) return fail(TVP_EINVAL, "tv1d_prox_fwd: NULL lam");
     if (n > tvp_max_line_1d(dt)) return fail(TVP_EUNSUPPORTED, "tv1d_prox_fwd: n > tvp_max_line_1d()");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    return dt == TVP_F32 ? tv1d_fwd_impl<float>(y, x, batch, n, stride, lam, lm, lam_scalar, mask, row_iters, s)
-                         : tv1d_fwd_impl<double>(y, x, batch, n, stride, lam, lm, lam_scalar, mask, row_iters, s);
+    return dt == TVP_F32
+               ? tv1d_fwd_impl<float>(y, x, batch, n, stride, lam, lm, lam_scalar, mask_out, row_iters, s, mask_in, o)
+               : tv1d_fwd_impl<double>(y, x, batch, n, stride, lam, lm, lam_scalar, mask_out, row_iters, s, mask_in, o);
+}
+
+extern "C" tvp_status_t tv1d_prox_fwd(tvp_dtype_t dt, const void* y, void* x, int64_t batch, int64_t n,
+                                      int64_t stride, const void* lam, tvp_lam_mode_t lm, double lam_scalar,
+                                      uint32_t* mask, int32_t* row_iters, tvp_stream_t stream) {
+    return tv1d_prox_fwd_ex(dt, y, x, batch, n, stride, lam, lm, lam_scalar, nullptr, mask, row_iters, nullptr,
+                            stream);
 }
 
 extern "C" tvp_status_t tv1d_prox_fwd_warm(tvp_dtype_t dt, const void* y, void* x, int64_t batch, int64_t n,
@@ -160,20 +206,8 @@ extern "C" tvp_status_t tv1d_prox_fwd_warm(tvp_dtype_t dt, const void* y, void* 
                                            const uint32_t* mask_in, uint32_t* mask_out, int32_t* row_iters,
                                            tvp_stream_t stream) {
     if (n > 1 && batch > 0 && !mask_in) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: NULL mask_in");
-    if (dt != TVP_F32 && dt != TVP_F64) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: bad dtype");
-    if (batch < 0 || n < 1 || stride < n) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: need batch >= 0, n >= 1, stride >= n");
-    if (lm != TVP_LAM_SCALAR && lm != TVP_LAM_PER_ROW && lm != TVP_LAM_PER_EDGE)
-        return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: lam mode must be SCALAR, PER_ROW or PER_EDGE");
-    if (lm == TVP_LAM_SCALAR && !(std::isfinite(lam_scalar) && lam_scalar >= 0.0))
-        return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: lam_scalar must be finite and >= 0");
-    if (batch == 0) return TVP_OK;
-    if (!y || !x) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: NULL y or x");
-    if (lm != TVP_LAM_SCALAR && !lam) return fail(TVP_EINVAL, "tv1d_prox_fwd_warm: NULL lam");
-    if (n > tvp_max_line_1d(dt)) return fail(TVP_EUNSUPPORTED, "tv1d_prox_fwd_warm: n > tvp_max_line_1d()");
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    return dt == TVP_F32
-               ? tv1d_fwd_impl<float>(y, x, batch, n, stride, lam, lm, lam_scalar, mask_out, row_iters, s, mask_in)
-               : tv1d_fwd_impl<double>(y, x, batch, n, stride, lam, lm, lam_scalar, mask_out, row_iters, s, mask_in);
+    return tv1d_prox_fwd_ex(dt, y, x, batch, n, stride, lam, lm, lam_scalar, mask_in, mask_out, row_iters, nullptr,
+                            stream);
 }
 
 template <typename T>
@@ -248,7 +282,7 @@ static bool lam2d_ok(tvp_lam_mode_t lm, const void* lam, double lam_scalar) {
 template <typename T>
 static tvp_status_t tv2d_fwd_impl(const void* Xv, void* Yv, int64_t N, int64_t C, int64_t H, int64_t W,
                                   const void* lam, tvp_lam_mode_t lm, double lam_scalar, int K, void* saved,
-                                  void* workspace, int32_t* line_iters, cudaStream_t s) {
+                                  void* workspace, int32_t* line_iters, cudaStream_t s, const Opts& o) {
     const int64_t planes = N * C;
     const Ws2D L = ws_layout(sizeof(T), N, C, H, W, K);
     char* ws = static_cast<char*>(workspace);
@@ -266,7 +300,7 @@ static tvp_status_t tv2d_fwd_impl(const void* Xv, void* Yv, int64_t N, int64_t C
         cudaError_t e = cudaMemsetAsync(line_iters, 0, sizeof(int32_t) * 2 * K, s);
         if (e != cudaSuccess) return cuda_status(e, "tv2d_prox_fwd");
     }
-    if (g_fused2d && plane_fwd_supported(H, W)) {
+    if (o.fused2d && plane_fwd_supported(H, W)) {
         // f2: the whole plane stays on chip for all K passes (no Z/P/Q workspace traffic)
         PlaneFwdArgs<T> f{};
         f.X = X;
@@ -283,7 +317,10 @@ static tvp_status_t tv2d_fwd_impl(const void* Xv, void* Yv, int64_t N, int64_t C
         f.mwr = (int)mwr;
         f.mwc = (int)mwc;
         f.iters_max = line_iters;
-        return cuda_status(launch_plane_fwd<T>(f, s), "tv2d_prox_fwd(fused)");
+        f.ls_after = o.ls_after;
+        f.diag = o.diag;
+        f.hist = o.hist;
+        return cuda_status(launch_plane_fwd<T>(f, s, o.lsp), "tv2d_prox_fwd(fused)");
     }
     for (int k = 1; k <= K; ++k) {
         // ---- row pass (Alg. 1 lines 3-6): Z = rowprox(Y + P); P <- (Y + P) - Z
@@ -305,7 +342,10 @@ static tvp_status_t tv2d_fwd_impl(const void* Xv, void* Yv, int64_t N, int64_t C
         r.mask_in = (k == 1) ? nullptr : (sv ? sv + (k - 2) * rset : rws);
         r.row_iters = nullptr;
         r.iters_max = line_iters ? line_iters + 2 * (k - 1) : nullptr;
-        cudaError_t e = launch_row_fwd<T>(r, false, true, s);
+        r.ls_after = o.ls_after;
+        r.diag = o.diag;
+        r.hist = o.hist ? o.hist + (int64_t)(2 * (k - 1)) * TVP_HIST_BINS : nullptr;
+        cudaError_t e = launch_row_fwd<T>(r, false, true, s, o.lsp);
         if (e != cudaSuccess) return cuda_status(e, "tv2d_prox_fwd(row)");
         // ---- column pass (lines 7-10): Y = colprox(Z + Q); Q <- (Z + Q) - Y
         ColFwdArgs<T> c{};
@@ -325,15 +365,21 @@ static tvp_status_t tv2d_fwd_impl(const void* Xv, void* Yv, int64_t N, int64_t C
         c.mask_out = sv ? cbase + (k - 1) * cset : cws;
         c.mask_in = (k == 1) ? nullptr : (sv ? cbase + (k - 2) * cset : cws);
         c.iters_max = line_iters ? line_iters + 2 * (k - 1) + 1 : nullptr;
-        e = launch_col_fwd<T>(c, s);
+        c.ls_after = o.ls_after;
+        c.diag = o.diag;
+        c.hist = o.hist ? o.hist + (int64_t)(2 * (k - 1) + 1) * TVP_HIST_BINS : nullptr;
+        e = launch_col_fwd<T>(c, s, o.lsp);
         if (e != cudaSuccess) return cuda_status(e, "tv2d_prox_fwd(col)");
     }
     return TVP_OK;
 }
 
-extern "C" tvp_status_t tv2d_prox_fwd(tvp_dtype_t dt, const void* X, void* Y, int64_t N, int64_t C, int64_t H,
-                                      int64_t W, const void* lam, tvp_lam_mode_t lm, double lam_scalar, int iters,
-                                      void* saved, void* workspace, int32_t* line_iters, tvp_stream_t stream) {
+extern "C" tvp_status_t tv2d_prox_fwd_ex(tvp_dtype_t dt, const void* X, void* Y, int64_t N, int64_t C, int64_t H,
+                                         int64_t W, const void* lam, tvp_lam_mode_t lm, double lam_scalar, int iters,
+                                         void* saved, void* workspace, int32_t* line_iters,
+                                         const tvp_options_t* opts, tvp_stream_t stream) {
+    Opts o;
+    if (!resolve_opts(opts, o)) return fail(TVP_EINVAL, "tv2d_prox_fwd: invalid tvp_options_t");
     if (dt != TVP_F32 && dt != TVP_F64) return fail(TVP_EINVAL, "tv2d_prox_fwd: bad dtype");
     if (N < 0 || C < 0 || H < 1 || W < 1 || iters < 1)
         return fail(TVP_EINVAL, "tv2d_prox_fwd: need N, C >= 0, H, W >= 1, iters >= 1");
@@ -343,13 +389,21 @@ extern "C" tvp_status_t tv2d_prox_fwd(tvp_dtype_t dt, const void* X, void* Y, in
     if (H > kMaxLine || W > kMaxLine) return fail(TVP_EUNSUPPORTED, "tv2d_prox_fwd: H or W > tvp_max_line()");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     return dt == TVP_F32
-               ? tv2d_fwd_impl<float>(X, Y, N, C, H, W, lam, lm, lam_scalar, iters, saved, workspace, line_iters, s)
-               : tv2d_fwd_impl<double>(X, Y, N, C, H, W, lam, lm, lam_scalar, iters, saved, workspace, line_iters, s);
+               ? tv2d_fwd_impl<float>(X, Y, N, C, H, W, lam, lm, lam_scalar, iters, saved, workspace, line_iters, s, o)
+               : tv2d_fwd_impl<double>(X, Y, N, C, H, W, lam, lm, lam_scalar, iters, saved, workspace, line_iters, s, o);
+}
+
+extern "C" tvp_status_t tv2d_prox_fwd(tvp_dtype_t dt, const void* X, void* Y, int64_t N, int64_t C, int64_t H,
+                                      int64_t W, const void* lam, tvp_lam_mode_t lm, double lam_scalar, int iters,
+                                      void* saved, void* workspace, int32_t* line_iters, tvp_stream_t stream) {
+    return tv2d_prox_fwd_ex(dt, X, Y, N, C, H, W, lam, lm, lam_scalar, iters, saved, workspace, line_iters, nullptr,
+                            stream);
 }
 
 template <typename T>
 static tvp_status_t tv2d_bwd_impl(const void* GYv, const void* saved, void* GXv, void* glam, int64_t N, int64_t C,
-                                  int64_t H, int64_t W, tvp_lam_mode_t lm, int K, void* workspace, cudaStream_t s) {
+                                  int64_t H, int64_t W, tvp_lam_mode_t lm, int K, void* workspace, cudaStream_t s,
+                                  const Opts& o) {
     const int64_t planes = N * C;
     const Ws2D L = ws_layout(sizeof(T), N, C, H, W, K);
     char* ws = static_cast<char*>(workspace);
@@ -361,7 +415,8 @@ static tvp_status_t tv2d_bwd_impl(const void* GYv, const void* saved, void* GXv,
     const T* G = static_cast<const T*>(GYv);
     T* GX = static_cast<T*>(GXv);
     const int64_t HW2 = H + W;
-    if (g_fused2d && plane_fwd_supported(H, W)) {
+    const bool fused = o.fused2d && plane_fwd_supported(H, W);
+    if (fused) {
         // f2: both adjoint planes stay on chip through all 2K adjoint passes
         PlaneBwdArgs<T> f{};
         f.G = G;
@@ -377,7 +432,7 @@ static tvp_status_t tv2d_bwd_impl(const void* GYv, const void* saved, void* GXv,
         cudaError_t e = launch_plane_bwd<T>(f, s);
         if (e != cudaSuccess) return cuda_status(e, "tv2d_prox_bwd(fused)");
     }
-    for (int k = K; k >= 1 && !(g_fused2d && plane_fwd_supported(H, W)); --k) {
+    for (int k = K; k >= 1 && !fused; --k) {
         // ---- column adjoint: r = A - B; B <- B + colsegmean_k(r)   (A = G at k = K, B = 0)
         ColBwdArgs<T> c{};
         c.A = (k == K) ? G : GX;
@@ -429,9 +484,12 @@ static tvp_status_t tv2d_bwd_impl(const void* GYv, const void* saved, void* GXv,
     return TVP_OK;
 }
 
-extern "C" tvp_status_t tv2d_prox_bwd(tvp_dtype_t dt, const void* grad_Y, const void* saved, void* grad_X,
-                                      void* grad_lam, int64_t N, int64_t C, int64_t H, int64_t W,
-                                      tvp_lam_mode_t lm, int iters, void* workspace, tvp_stream_t stream) {
+extern "C" tvp_status_t tv2d_prox_bwd_ex(tvp_dtype_t dt, const void* grad_Y, const void* saved, void* grad_X,
+                                         void* grad_lam, int64_t N, int64_t C, int64_t H, int64_t W,
+                                         tvp_lam_mode_t lm, int iters, void* workspace, const tvp_options_t* opts,
+                                         tvp_stream_t stream) {
+    Opts o;
+    if (!resolve_opts(opts, o)) return fail(TVP_EINVAL, "tv2d_prox_bwd: invalid tvp_options_t");
     if (dt != TVP_F32 && dt != TVP_F64) return fail(TVP_EINVAL, "tv2d_prox_bwd: bad dtype");
     if (N < 0 || C < 0 || H < 1 || W < 1 || iters < 1)
         return fail(TVP_EINVAL, "tv2d_prox_bwd: need N, C >= 0, H, W >= 1, iters >= 1");
@@ -447,8 +505,14 @@ extern "C" tvp_status_t tv2d_prox_bwd(tvp_dtype_t dt, const void* grad_Y, const 
     }
     if (!grad_Y || !grad_X || !workspace || !saved) return fail(TVP_EINVAL, "tv2d_prox_bwd: NULL grad_Y, grad_X, saved or workspace");
     if (H > kMaxLine || W > kMaxLine) return fail(TVP_EUNSUPPORTED, "tv2d_prox_bwd: H or W > tvp_max_line()");
-    return dt == TVP_F32 ? tv2d_bwd_impl<float>(grad_Y, saved, grad_X, grad_lam, N, C, H, W, lm, iters, workspace, s)
-                         : tv2d_bwd_impl<double>(grad_Y, saved, grad_X, grad_lam, N, C, H, W, lm, iters, workspace, s);
+    return dt == TVP_F32 ? tv2d_bwd_impl<float>(grad_Y, saved, grad_X, grad_lam, N, C, H, W, lm, iters, workspace, s, o)
+                         : tv2d_bwd_impl<double>(grad_Y, saved, grad_X, grad_lam, N, C, H, W, lm, iters, workspace, s, o);
+}
+
+extern "C" tvp_status_t tv2d_prox_bwd(tvp_dtype_t dt, const void* grad_Y, const void* saved, void* grad_X,
+                                      void* grad_lam, int64_t N, int64_t C, int64_t H, int64_t W,
+                                      tvp_lam_mode_t lm, int iters, void* workspace, tvp_stream_t stream) {
+    return tv2d_prox_bwd_ex(dt, grad_Y, saved, grad_X, grad_lam, N, C, H, W, lm, iters, workspace, nullptr, stream);
 }
 
 // ------------------------------------------------------------ TV layer (f1)
@@ -483,7 +547,8 @@ static tvp_status_t lines_fwd_impl(const void* X, void* Y, int64_t N, int64_t C,
         a.C = (int)(C > 0 ? C : 1);
         a.mask_out = mask;
         a.mw = (int)mask_words(W);
-        return cuda_status(launch_row_fwd<T>(a, false, false, s), "tv2d_lines_fwd(rows)");
+        a.ls_after = kLsAfterDefault;
+        return cuda_status(launch_row_fwd<T>(a, false, false, s, false), "tv2d_lines_fwd(rows)");
     }
     ColFwdArgs<T> c{};
     c.Z = static_cast<const T*>(X);
@@ -497,7 +562,8 @@ static tvp_status_t lines_fwd_impl(const void* X, void* Y, int64_t N, int64_t C,
     c.W = (int)W;
     c.mask_out = mask;
     c.mw = (int)mask_words(H);
-    return cuda_status(launch_col_fwd<T>(c, s), "tv2d_lines_fwd(cols)");
+    c.ls_after = kLsAfterDefault;
+    return cuda_status(launch_col_fwd<T>(c, s, false), "tv2d_lines_fwd(cols)");
 }
 
 extern "C" tvp_status_t tv2d_lines_fwd(tvp_dtype_t dt, const void* X, void* Y, int64_t N, int64_t C, int64_t H,
@@ -574,7 +640,14 @@ extern "C" tvp_status_t tv2d_lines_bwd(tvp_dtype_t dt, const void* grad_Y, const
     if (!lines_args_ok(N, C, H, W, axis)) return fail(TVP_EINVAL, "tv2d_lines_bwd: need N, C >= 0, H, W >= 1, axis 0/1");
     if (lm != TVP_LAM_SCALAR && lm != TVP_LAM_PER_CHANNEL && lm != TVP_LAM_PER_PLANE)
         return fail(TVP_EINVAL, "tv2d_lines_bwd: lam mode must be SCALAR, PER_CHANNEL or PER_PLANE");
-    if (N * C == 0) return TVP_OK;
+    if (N * C == 0) {
+        // an empty batch contributes nothing: the lambda gradient is zero (1 or C entries)
+        const size_t cnt = lm == TVP_LAM_SCALAR ? 1 : (lm == TVP_LAM_PER_CHANNEL ? (size_t)C : 0);
+        if (grad_lam && cnt)
+            return cuda_status(cudaMemsetAsync(grad_lam, 0, cnt * (dt == TVP_F64 ? 8 : 4),
+                                               reinterpret_cast<cudaStream_t>(stream)), "tv2d_lines_bwd");
+        return TVP_OK;
+    }
     const int64_t L = axis == 0 ? W : H;
     if (!grad_Y || !grad_X || (L > 1 && !mask)) return fail(TVP_EINVAL, "tv2d_lines_bwd: NULL grad_Y, grad_X or mask");
     if (grad_lam && !workspace) return fail(TVP_EINVAL, "tv2d_lines_bwd: NULL workspace");

@@ -39,6 +39,24 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+def make_options(fused2d: int = -1, line_search: str = "backtrack", ls_after: int = 0, diag: torch.Tensor = None,
+                 iter_hist: torch.Tensor = None):
+    """tvp_options_t for the *_ex calls (include/tvprox.h).  diag: int32 CUDA [4];
+    iter_hist: int32 CUDA [passes, HIST_BINS] (both accumulated by the call)."""
+    ls = {"backtrack": _lib.LS_BACKTRACK, "parallel": _lib.LS_PARALLEL}[line_search]
+    for t in (diag, iter_hist):
+        if t is not None:
+            _require_cuda(t)
+            if t.dtype != torch.int32 or not t.is_contiguous():
+                raise ValueError("tvprox: diag / iter_hist must be contiguous int32")
+    return _lib.Options(int(fused2d), ls, int(ls_after), _ptr(diag), _ptr(iter_hist))
+
+
+def _opts_ref(opts):
+    import ctypes
+    return None if opts is None else ctypes.byref(opts)
+
+
 def _rows(y: torch.Tensor) -> torch.Tensor:
     if y.dim() != 2:
         raise ValueError("tvprox: 1D input must be [batch, n]")
@@ -71,9 +89,10 @@ def _lam1d(lam, y: torch.Tensor):
 
 
 def tv1d_fwd(y: torch.Tensor, lam, need_mask: bool = True, want_iters: bool = False,
-             warm_mask: torch.Tensor = None):
+             warm_mask: torch.Tensor = None, opts=None):
     """Batched 1D TV prox forward.  Returns (x, mask or None, row_iters or None).
-    warm_mask: optional saved mask of a previous solve to warm-start projected Newton."""
+    warm_mask: optional saved mask of a previous solve to warm-start projected Newton.
+    opts: optional make_options(...) (line-search flavour, diagnostics)."""
     _require_cuda(y)
     y = _rows(y)
     dt = _dtype_code(y)
@@ -89,6 +108,10 @@ def tv1d_fwd(y: torch.Tensor, lam, need_mask: bool = True, want_iters: bool = Fa
     it = torch.empty(b, device=y.device, dtype=torch.int32) if want_iters else None
     if warm_mask is not None:
         _require_cuda(warm_mask)
+    if opts is not None:
+        check(lib.tv1d_prox_fwd_ex(dt, _ptr(y), _ptr(x), b, n, stride, _ptr(lt), mode, scal, _ptr(warm_mask),
+                                   _ptr(mask), _ptr(it), _opts_ref(opts), _stream(y)), "tv1d_prox_fwd_ex")
+    elif warm_mask is not None:
         check(lib.tv1d_prox_fwd_warm(dt, _ptr(y), _ptr(x), b, n, stride, _ptr(lt), mode, scal,
                                      _ptr(warm_mask), _ptr(mask), _ptr(it), _stream(y)), "tv1d_prox_fwd_warm")
     else:
@@ -132,6 +155,8 @@ class TV1DProx(torch.autograd.Function):
         ctx.save_for_backward(mask)
         ctx.mode = mode
         ctx.lam_shape = None if lam_t is None else lam_t.shape
+        ctx.lam_device = None if lam_t is None else lam_t.device
+        ctx.lam_dtype = None if lam_t is None else lam_t.dtype
         return x
 
     @staticmethod
@@ -140,8 +165,21 @@ class TV1DProx(torch.autograd.Function):
         need_lam = ctx.needs_input_grad[1]
         gy, gl = tv1d_bwd(gx.contiguous(), mask, ctx.mode, want_lam=need_lam)
         if need_lam and gl is not None and ctx.lam_shape is not None:
-            gl = gl.reshape(ctx.lam_shape) if gl.numel() == int(torch.Size(ctx.lam_shape).numel()) else gl
+            gl = _lam_grad_like(gl, ctx.lam_shape, ctx.lam_device, ctx.lam_dtype)
         return gy, (gl if need_lam else None), None
+
+
+def _lam_grad_like(gl: torch.Tensor, shape, device, dtype) -> torch.Tensor:
+    """The lambda gradient in the caller's lambda layout: per-edge lambda given as
+    [batch, n] or [batch, pitch] gets zeros beyond edge n-2 (those entries are not used),
+    and the gradient lives on lambda's own device and dtype."""
+    shape = torch.Size(shape)
+    if gl.numel() != shape.numel():
+        full = torch.zeros(shape, device=gl.device, dtype=gl.dtype)
+        m = min(full.shape[-1], gl.shape[-1])
+        full[..., :m] = gl.reshape(full.shape[0], -1)[:, :m]
+        gl = full
+    return gl.reshape(shape).to(device=device, dtype=dtype)
 
 
 def tv1d(y: torch.Tensor, lam) -> torch.Tensor:
@@ -166,8 +204,10 @@ def _lam2d(lam, X: torch.Tensor):
     raise ValueError("tvprox: 2D lam must be a float, [C] or [N, C]")
 
 
-def tv2d_fwd(X: torch.Tensor, lam, iters: int = 4, training: bool = True, want_iters: bool = False):
-    """Returns (Y, saved or None, line_iters or None)."""
+def tv2d_fwd(X: torch.Tensor, lam, iters: int = 4, training: bool = True, want_iters: bool = False, opts=None,
+             out: torch.Tensor = None):
+    """Returns (Y, saved or None, line_iters or None).  opts: optional make_options(...);
+    out: optional output tensor (may be X itself: in-place)."""
     _require_cuda(X)
     if X.dim() != 4:
         raise ValueError("tvprox: 2D input must be NCHW")
@@ -176,7 +216,11 @@ def tv2d_fwd(X: torch.Tensor, lam, iters: int = 4, training: bool = True, want_i
     lib = _lib.load()
     N, C, H, W = X.shape
     mode, scal, lt = _lam2d(lam, X)
-    Y = torch.empty_like(X)
+    if out is not None:
+        _require_cuda(out)
+        if out.shape != X.shape or out.dtype != X.dtype or not out.is_contiguous():
+            raise ValueError("tvprox: out must be a contiguous tensor like X")
+    Y = torch.empty_like(X) if out is None else out
     saved = None
     if training:
         sb = lib.tv2d_saved_bytes(N, C, H, W, iters)
@@ -184,27 +228,40 @@ def tv2d_fwd(X: torch.Tensor, lam, iters: int = 4, training: bool = True, want_i
     wsb = lib.tv2d_workspace_bytes(dt, N, C, H, W, iters)
     ws = torch.empty(max(wsb, 1), device=X.device, dtype=torch.uint8)
     it = torch.empty(2 * iters, device=X.device, dtype=torch.int32) if want_iters else None
-    check(lib.tv2d_prox_fwd(dt, _ptr(X), _ptr(Y), N, C, H, W, _ptr(lt), mode, scal, int(iters),
-                            _ptr(saved), _ptr(ws), _ptr(it), _stream(X)), "tv2d_prox_fwd")
+    if opts is not None:
+        check(lib.tv2d_prox_fwd_ex(dt, _ptr(X), _ptr(Y), N, C, H, W, _ptr(lt), mode, scal, int(iters),
+                                   _ptr(saved), _ptr(ws), _ptr(it), _opts_ref(opts), _stream(X)), "tv2d_prox_fwd_ex")
+    else:
+        check(lib.tv2d_prox_fwd(dt, _ptr(X), _ptr(Y), N, C, H, W, _ptr(lt), mode, scal, int(iters),
+                                _ptr(saved), _ptr(ws), _ptr(it), _stream(X)), "tv2d_prox_fwd")
     return Y, saved, it
 
 
-def tv2d_bwd(grad_Y: torch.Tensor, saved: torch.Tensor, lam_mode: int, iters: int, want_lam: bool = True):
-    """Returns (grad_X, grad_lam or None)."""
+def tv2d_bwd(grad_Y: torch.Tensor, saved: torch.Tensor, lam_mode: int, iters: int, want_lam: bool = True,
+             opts=None, out: torch.Tensor = None):
+    """Returns (grad_X, grad_lam or None).  out: optional grad_X tensor (may be grad_Y: in-place)."""
     _require_cuda(grad_Y, saved)
     G = grad_Y.contiguous()
     dt = _dtype_code(G)
     lib = _lib.load()
     N, C, H, W = G.shape
-    GX = torch.empty_like(G)
+    if out is not None:
+        _require_cuda(out)
+        if out.shape != G.shape or out.dtype != G.dtype or not out.is_contiguous():
+            raise ValueError("tvprox: out must be a contiguous tensor like grad_Y")
+    GX = torch.empty_like(G) if out is None else out
     glam = None
     if want_lam:
         cnt = {_lib.LAM_SCALAR: 1, _lib.LAM_PER_CHANNEL: C, _lib.LAM_PER_PLANE: N * C}[lam_mode]
         glam = torch.empty(max(cnt, 1), device=G.device, dtype=G.dtype)
     wsb = lib.tv2d_workspace_bytes(dt, N, C, H, W, iters)
     ws = torch.empty(max(wsb, 1), device=G.device, dtype=torch.uint8)
-    check(lib.tv2d_prox_bwd(dt, _ptr(G), _ptr(saved), _ptr(GX), _ptr(glam), N, C, H, W, lam_mode,
-                            int(iters), _ptr(ws), _stream(G)), "tv2d_prox_bwd")
+    if opts is not None:
+        check(lib.tv2d_prox_bwd_ex(dt, _ptr(G), _ptr(saved), _ptr(GX), _ptr(glam), N, C, H, W, lam_mode,
+                                   int(iters), _ptr(ws), _opts_ref(opts), _stream(G)), "tv2d_prox_bwd_ex")
+    else:
+        check(lib.tv2d_prox_bwd(dt, _ptr(G), _ptr(saved), _ptr(GX), _ptr(glam), N, C, H, W, lam_mode,
+                                int(iters), _ptr(ws), _stream(G)), "tv2d_prox_bwd")
     return GX, glam
 
 
@@ -217,6 +274,8 @@ class TV2DProx(torch.autograd.Function):
         ctx.save_for_backward(saved)
         ctx.mode, ctx.iters = mode, iters
         ctx.lam_shape = None if lam_t is None else lam_t.shape
+        ctx.lam_device = None if lam_t is None else lam_t.device
+        ctx.lam_dtype = None if lam_t is None else lam_t.dtype
         return Y
 
     @staticmethod
@@ -225,7 +284,7 @@ class TV2DProx(torch.autograd.Function):
         need_lam = ctx.needs_input_grad[1]
         gX, gl = tv2d_bwd(gY, saved, ctx.mode, ctx.iters, want_lam=need_lam)
         if need_lam and gl is not None and ctx.lam_shape is not None:
-            gl = gl.reshape(ctx.lam_shape)
+            gl = gl.reshape(ctx.lam_shape).to(device=ctx.lam_device, dtype=ctx.lam_dtype)
         return gX, (gl if need_lam else None), None, None
 
 
@@ -283,6 +342,8 @@ class TVLinesProx(torch.autograd.Function):
         ctx.save_for_backward(mask)
         ctx.mode, ctx.axis = mode, axis
         ctx.lam_shape = None if lam_t is None else lam_t.shape
+        ctx.lam_device = None if lam_t is None else lam_t.device
+        ctx.lam_dtype = None if lam_t is None else lam_t.dtype
         return Y
 
     @staticmethod
@@ -291,7 +352,7 @@ class TVLinesProx(torch.autograd.Function):
         need_lam = ctx.needs_input_grad[1]
         gX, gl = tv2d_lines_bwd(gY, mask, ctx.mode, ctx.axis, want_lam=need_lam)
         if need_lam and gl is not None and ctx.lam_shape is not None:
-            gl = gl.reshape(ctx.lam_shape)
+            gl = gl.reshape(ctx.lam_shape).to(device=ctx.lam_device, dtype=ctx.lam_dtype)
         return gX, (gl if need_lam else None), None, None
 
 

@@ -9,7 +9,8 @@ Recipe (DESIGN.md "Input recipe"):
   C1 (BJ:7)   1D fp64, 8 x 64, lam 0.5; rows 0-3 unit step at 32 + N(0, 0.1^2)
               (Table 1 family), rows 4-7 iid N(0,1)
   C2 (BJ:8)   1D fp32, 65536 x 1024, per-row lam = softplus(U(-2,1));
-              unit step at 512 + N(0, sigma_b^2), sigma 0.1 (even b) / 0.5 (odd b)
+              unit step at 512 + N(0, sigma_b^2), sigma 0.1 (even b) / 0.5 (odd b);
+              seeded per block of 1024 rows ([seed, block]) so row shards are slices
   C3 (BJ:9)   2D fp32 NCHW 64x64x56x56, K=4, per-channel lam =
               softplus(linspace(-3, 0, 64)); X = max(N(0,1), 0) (post-ReLU features)
   C4 (BJ:10)  2D fp32 16x3x512x512, K=4, scalar lam = 1; per plane a background
@@ -94,15 +95,27 @@ def c1(with_grad=True) -> Workload1D:
     return Workload1D("C1", y.astype(np.float64), np.full(8, 0.5), "scalar", 0.5, "f64", seed, g)
 
 
-def c2(batch=65536, n=1024, with_grad=True, dtype=np.float32) -> Workload1D:
+C2_BLOCK = 1024       # rows per seeding block of C2 (so any row shard is reproducible)
+
+
+def c2(batch=65536, n=1024, with_grad=True, dtype=np.float32, row_offset=0) -> Workload1D:
+    """Rows [row_offset, row_offset + batch) of the C2 family.  Row block j (C2_BLOCK rows)
+    draws from its own streams [seed + {0,1,2}, j], so a rank's shard of a multi-GPU batch
+    equals the same rows of the single-GPU batch (the N-GPU verification compares them)."""
     seed = 1000 * 2
-    rng = np.random.default_rng(seed + 0)
-    sig = np.where(np.arange(batch) % 2 == 0, 0.1, 0.5)
-    y = _unit_step(rng, batch, n, n // 2, sig).astype(dtype)
-    lt = np.random.default_rng(seed + 1).uniform(-2.0, 1.0, size=batch)
-    lam = softplus_np(lt).astype(dtype).astype(np.float64)
-    g = (np.random.default_rng(seed + 2).standard_normal((batch, n)).astype(dtype)
-         if with_grad else None)
+    b0, b1 = row_offset // C2_BLOCK, (row_offset + batch + C2_BLOCK - 1) // C2_BLOCK
+    ys, lts, gs = [], [], []
+    for j in range(b0, b1):
+        rows = np.arange(j * C2_BLOCK, (j + 1) * C2_BLOCK)
+        sig = np.where(rows % 2 == 0, 0.1, 0.5)
+        ys.append(_unit_step(np.random.default_rng([seed + 0, j]), C2_BLOCK, n, n // 2, sig).astype(dtype))
+        lts.append(np.random.default_rng([seed + 1, j]).uniform(-2.0, 1.0, size=C2_BLOCK))
+        if with_grad:
+            gs.append(np.random.default_rng([seed + 2, j]).standard_normal((C2_BLOCK, n)).astype(dtype))
+    lo = row_offset - b0 * C2_BLOCK
+    y = np.ascontiguousarray(np.concatenate(ys)[lo:lo + batch])
+    lam = softplus_np(np.concatenate(lts)[lo:lo + batch]).astype(dtype).astype(np.float64)
+    g = np.ascontiguousarray(np.concatenate(gs)[lo:lo + batch]) if with_grad else None
     return Workload1D("C2", y, lam, "row", 0.0, "f32", seed, g)
 
 

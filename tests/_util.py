@@ -39,3 +39,50 @@ def rel_err(a, b, ref_range):
 def rng_range(x):
     x = np.asarray(x, np.float64)
     return float(x.max() - x.min()) if x.size else 0.0
+
+
+def _spread(taint, brk):
+    """Any tainted sample of a segment (breaks brk [L, n-1] != 0) taints the whole segment."""
+    L, n = taint.shape
+    if n == 0:
+        return taint.copy()
+    seg = np.zeros((L, n), np.int64)
+    if n > 1:
+        seg[:, 1:] = np.cumsum(brk != 0, axis=1)
+    ids = seg + (np.arange(L, dtype=np.int64)[:, None] * n)
+    cnt = np.bincount(ids.ravel(), weights=taint.ravel().astype(np.float64), minlength=L * n)
+    return cnt[ids] > 0
+
+
+def taint_2d(gpu_segs, ref_segs, H, W, K):
+    """Pixels of each plane whose 2D adjoint (reverse mode through Alg. 1, a-14) can depend
+    on a mask disagreement between two segmentations (reading O13 (ii) in 2D).
+
+    segs = (rbrk [P][K][H][W-1], rsgn, cbrk [P][K][W][H-1], csgn).  Reverse order
+    k = K..1: column adjoint, then row adjoint.  A pass seeds both samples of every edge
+    whose break flag differs, and the output of a segment-mean pass at a pixel can differ
+    when that pixel's segment under EITHER segmentation holds a tainted input.
+    Returns a bool array [P, H, W]."""
+    grb, _, gcb, _ = gpu_segs
+    orb, _, ocb, _ = ref_segs
+    P = grb.shape[0]
+    out = np.zeros((P, H, W), bool)
+    for p in range(P):
+        t = np.zeros((H, W), bool)
+        for k in range(K - 1, -1, -1):
+            # column adjoint k (lines = columns)
+            tc = t.T.copy()
+            if H > 1:
+                d = gcb[p, k] != ocb[p, k]
+                tc[:, :-1] |= d
+                tc[:, 1:] |= d
+            tc = _spread(tc, gcb[p, k]) | _spread(tc, ocb[p, k])
+            t = tc.T.copy()
+            # row adjoint k
+            if W > 1:
+                d = grb[p, k] != orb[p, k]
+                t[:, :-1] |= d
+                t[:, 1:] |= d
+            t = _spread(t, grb[p, k]) | _spread(t, orb[p, k])
+        out[p] = t
+    return out

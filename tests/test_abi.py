@@ -57,6 +57,7 @@ def test_size_queries(lib):
     assert lib.tv1d_bwd_workspace_bytes(0, 100, 0) >= 400
     assert lib.tv1d_bwd_workspace_bytes(0, 100, 1) == 0
     assert lib.tvp_version() >= 100
+    assert lib.tvp_max_line(1) >= 1024
 
 
 def test_invalid_arguments_rejected_before_launch(lib):
@@ -86,3 +87,37 @@ def test_invalid_arguments_rejected_before_launch(lib):
     msg = lib.tvp_last_error().decode()
     assert "tv2d_prox_bwd" in msg
     assert b"EINVAL" in lib.tvp_status_string(E)
+
+
+def test_options_validated_and_defaulted(lib):
+    """tvp_options_t (per-call options): defaults, and invalid values rejected before any launch."""
+    import ctypes as ct
+    from paper_2204_03643_b200 import _lib
+    o = _lib.Options(7, 7, 7, None, None)
+    lib.tvp_options_default(ct.byref(o))
+    assert (o.fused2d, o.line_search, o.ls_after, o.diag, o.iter_hist) == (-1, _lib.LS_BACKTRACK, 0, None, None)
+    fake = ct.c_void_p(16)
+    E = _lib.TVP_EINVAL
+    for bad in (_lib.Options(2, 0, 0, None, None), _lib.Options(-2, 0, 0, None, None),
+                _lib.Options(-1, 2, 0, None, None), _lib.Options(-1, 0, -1, None, None)):
+        assert lib.tv1d_prox_fwd_ex(0, fake, fake, 4, 8, 8, None, 0, 0.5, None, None, None, ct.byref(bad), None) == E
+        assert lib.tv2d_prox_fwd_ex(0, fake, fake, 1, 1, 4, 4, None, 0, 0.5, 4, None, fake, None, ct.byref(bad),
+                                    None) == E
+        assert lib.tv2d_prox_bwd_ex(0, fake, fake, fake, None, 1, 1, 4, 4, 0, 4, fake, ct.byref(bad), None) == E
+    assert "tvp_options_t" in lib.tvp_last_error().decode()
+    ok = _lib.Options(1, 1, 2, None, None)
+    # valid options, empty batch: OK without touching the (fake) buffers
+    assert lib.tv1d_prox_fwd_ex(0, fake, fake, 0, 8, 8, None, 0, 0.5, None, None, None, ct.byref(ok), None) == 0
+    assert lib.tv2d_prox_fwd_ex(0, fake, fake, 0, 3, 4, 4, None, 0, 0.5, 4, None, fake, None, ct.byref(ok), None) == 0
+
+
+def test_fused2d_default_is_thread_local(lib):
+    """tvp_set_fused2d sets the CALLING thread's default only (no process-global state)."""
+    import threading
+    prev = lib.tvp_set_fused2d(0)
+    seen = []
+    t = threading.Thread(target=lambda: seen.append(lib.tvp_set_fused2d(1)))
+    t.start()
+    t.join()
+    assert seen == [1]                         # the other thread still had the initial default
+    assert lib.tvp_set_fused2d(prev) == 0      # ours was not changed by the other thread

@@ -125,3 +125,56 @@ def test_layer_identity_at_zero_lambda(mods):
         L = layer.TVLayer(3, is_sharp=sharp, init=-200.0, device="cuda")
         Y = L(X)
         assert torch.equal(Y, X) or torch.allclose(Y, X, atol=0, rtol=0)
+
+
+def test_per_edge_lambda_grad_layouts(mods):
+    """A per-edge lambda given as [batch, n] (the last column unused) gets a gradient of the
+    same shape with zeros there; a CPU lambda gets its gradient on the CPU."""
+    tp, _ = mods
+    rng = np.random.default_rng(12)
+    y = torch.tensor(rng.standard_normal((6, 40)), device="cuda", requires_grad=True)
+    lam_full = torch.tensor(rng.uniform(0.1, 1.0, (6, 40)), device="cuda", requires_grad=True)
+    x = tp.tv1d(y, lam_full)
+    g = torch.tensor(rng.standard_normal((6, 40)), device="cuda")
+    (x * g).sum().backward()
+    assert lam_full.grad.shape == (6, 40)
+    assert torch.all(lam_full.grad[:, -1] == 0)
+    # same values as the [batch, n-1] form
+    lam_e = lam_full.detach()[:, :39].clone().requires_grad_(True)
+    y2 = y.detach().clone().requires_grad_(True)
+    (tp.tv1d(y2, lam_e) * g).sum().backward()
+    assert torch.allclose(lam_full.grad[:, :39], lam_e.grad)
+    # CPU per-row lambda: gradient comes back on the CPU, same values
+    lam_cpu = torch.tensor(rng.uniform(0.1, 1.0, 6), requires_grad=True)
+    y3 = y.detach().clone().requires_grad_(True)
+    (tp.tv1d(y3, lam_cpu) * g).sum().backward()
+    assert lam_cpu.grad.device.type == "cpu" and lam_cpu.grad.shape == (6,)
+    lam_gpu = lam_cpu.detach().cuda().requires_grad_(True)
+    (tp.tv1d(y.detach(), lam_gpu) * g).sum().backward()
+    assert torch.allclose(lam_cpu.grad, lam_gpu.grad.cpu())
+    # 2D, CPU per-channel lambda
+    X = torch.tensor(rng.standard_normal((2, 3, 20, 30)), device="cuda", requires_grad=True)
+    lc = torch.tensor([0.2, 0.4, 0.8], requires_grad=True)
+    (tp.tv2d(X, lc, iters=2) * torch.ones_like(X[:1])).sum().backward()
+    assert lc.grad.device.type == "cpu" and lc.grad.shape == (3,)
+
+
+def test_layer_default_init_and_shared_lambda(mods):
+    """TVLayer initialises lambda = 0.05; shared=True learns one lambda for all
+    channels ("lambda shared across channels") through the per-channel kernels."""
+    tp, layer = mods
+    L = layer.TVLayer(num_chan=4, device="cuda")
+    assert torch.allclose(L.lam, torch.full((4,), 0.05, device="cuda"), atol=1e-6)
+    Ls = layer.TVLayer(num_chan=4, shared=True, init=0.3, dtype=torch.float64, device="cuda")
+    assert Ls._lmbd.shape == (1,)
+    rng = np.random.default_rng(3)
+    X = torch.tensor(rng.standard_normal((2, 4, 24, 24)), device="cuda", requires_grad=True)
+    Y = Ls(X)
+    G = torch.tensor(rng.standard_normal(Y.shape), device="cuda")
+    (Y * G).sum().backward()
+    lam = float(np.log1p(np.exp(0.3)))
+    Yr, segs = oracle.prox2d_batch(X.detach().cpu().numpy().reshape(8, 24, 24), np.full(8, lam), 4)
+    assert np.abs(Y.detach().cpu().numpy().reshape(8, 24, 24) - Yr).max() <= 1e-9 * rng_range(Yr)
+    _, glr = oracle.bwd2d_batch(segs, G.cpu().numpy().reshape(8, 24, 24), 4)
+    sig = 1.0 / (1.0 + np.exp(-0.3))
+    assert abs(Ls._lmbd.grad.item() - glr.sum() * sig) <= 1e-9 * (np.abs(glr).sum() + 1)

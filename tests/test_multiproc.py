@@ -67,3 +67,66 @@ def test_shard_edges():
             for off, c in got:
                 assert off == pos
                 pos += c
+
+
+def _verify_worker(rank, ws, port, q):
+    """bench.py's verification plumbing on gloo: each rank computes a deterministic per-row
+    function of ITS C2 shard (rows [r*B, (r+1)*B) of the block-seeded global batch), the
+    shards are all-gathered to rank 0 and compared bitwise with the same function of the
+    whole batch; a tampered shard must be caught."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import bench
+    from paper_2204_03643_b200 import workloads
+    B, n = 1500, 64                       # not a multiple of the 1024-row seeding block
+
+    def f(y, lam):                        # any deterministic row-wise map stands in for the solver
+        x = torch.cumsum(torch.as_tensor(y, dtype=torch.float64), dim=1) * torch.as_tensor(lam)[:, None]
+        return {"x": x.float(), "mask": (x > 0).to(torch.int32), "lam": torch.as_tensor(lam, dtype=torch.float32)}
+
+    w = workloads.c2(batch=B, n=n, row_offset=rank * B)
+    local = f(w.y, w.lam)
+    res = {}
+    g = bench.gather_to_rank0(local, ws, rank)
+    if rank == 0:
+        full = workloads.c2(batch=B * ws, n=n)
+        res["ok"] = bench.bitwise_compare(g, f(full.y, full.lam), tolerant=("lam",))
+    bad = dict(local)
+    if rank == 1:
+        bad["x"] = bad["x"].clone()
+        bad["x"][7, 3] = torch.nextafter(bad["x"][7, 3], torch.tensor(1e9))
+    g2 = bench.gather_to_rank0(bad, ws, rank)
+    if rank == 0:
+        res["bad"] = bench.bitwise_compare(g2, f(full.y, full.lam))
+    q.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gather_verify():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_verify_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ok, bad = res[0]["ok"], res[0]["bad"]
+    assert ok["x"] is True and ok["mask"] is True
+    assert ok["lam"]["max_abs_diff"] == 0.0
+    assert bad["x"] is False and bad["mask"] is True
+
+
+def test_gpus_flag_mismatch_is_an_error():
+    """bench.py --gpus N under a launcher whose WORLD_SIZE differs must refuse to run."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4"], env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert p.returncode != 0 and "WORLD_SIZE=2" in p.stderr

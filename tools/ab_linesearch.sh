@@ -6,18 +6,18 @@
 #   on the GPU:  bash tools/ab_linesearch.sh run     (timings + the full -m gpu suite per variant)
 set -e
 if [ "$1" == "build" ]; then
-  mkdir -p scratch/libs
+  mkdir -p build_ab
   B="python -m paper_2204_03643_b200.build"
-  $B --define TVP_LS_AFTER=1 --out scratch/libs/ls_backtrack.so &
-  $B --define TVP_LS_AFTER=1 --define TVP_LS_PARALLEL=1 --out scratch/libs/ls_parallel.so &
+  $B --define TVP_LS_AFTER=1 --out build_ab/ls_backtrack.so &
+  $B --define TVP_LS_AFTER=1 --define TVP_LS_PARALLEL=1 --out build_ab/ls_parallel.so &
   $B > /dev/null; wait
-  cp paper_2204_03643_b200/libtvprox.so scratch/libs/default.so
+  cp paper_2204_03643_b200/libtvprox.so build_ab/default.so
   rm -rf paper_2204_03643_b200/build_*
 else
   bash tools/ab.sh c2 c5
   cp paper_2204_03643_b200/libtvprox.so /tmp/keep.so
   for v in ls_backtrack ls_parallel; do
-    cp scratch/libs/$v.so paper_2204_03643_b200/libtvprox.so
+    cp build_ab/$v.so paper_2204_03643_b200/libtvprox.so
     echo "$v: $(python -m pytest tests -m gpu -x -q 2>&1 | tail -1)"
   done
   cp /tmp/keep.so paper_2204_03643_b200/libtvprox.so

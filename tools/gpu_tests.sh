@@ -1,0 +1,6 @@
+set -x
+nvidia-smi -L
+python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 -rf > gpurun_out/t1.log 2>&1
+echo "pytest rc=$?"
+tail -30 gpurun_out/t1.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke1.log 2>&1; echo "smoke rc=$?"; tail -3 gpurun_out/smoke1.log
