@@ -437,7 +437,7 @@ def time_1d_config(w, dev, ws, reps, flush, peak):
             "scaling": "weak (replicated per rank)"}
 
 
-def time_2d_config(w, dev, ws, reps, flush, peak, graph=True):
+def time_2d_config(w, dev, ws, reps, flush, peak, graph=True, cluster=False):
     """2D config: fwd (training, saved masks) and bwd (with lambda gradient) timed
     separately with an L2 flush before each, eager and as CUDA graphs; per-pass PN
     iteration statistics from the iteration histogram."""
@@ -487,6 +487,15 @@ def time_2d_config(w, dev, ws, reps, flush, peak, graph=True):
             GXg, glg = bwd(sg)
         gfm, gbm = run(lambda: gf.replay(), lambda s: gb.replay())
         out["graph"] = {"fwd_ms": stats_ms(gfm), "bwd_ms": stats_ms(gbm)}
+    if cluster:
+        # f2 on a thread-block cluster (tvp_options_t.fused2d = 1): on-chip plane state, bitwise
+        # the same result; reported beside the default (staged) path it is measured against
+        oc = tvprox.make_options(fused2d=1)
+        Yc, sc, _ = tvprox.tv2d_fwd(X, lam, K, training=True, opts=oc)
+        cf, cb = run(lambda: tvprox.tv2d_fwd(X, lam, K, training=True, opts=oc)[1],
+                     lambda s: tvprox.tv2d_bwd(G, s, mode, K, want_lam=True, opts=oc))
+        out["cluster_f2"] = {"fwd_ms": stats_ms(cf), "bwd_ms": stats_ms(cb),
+                             "bitwise_equal_to_default": bool(torch.equal(Yc, Y) and torch.equal(sc, saved))}
     hist = torch.zeros((2 * K, _lib.HIST_BINS), dtype=torch.int32, device=dev)
     tvprox.tv2d_fwd(X, lam, K, training=False, opts=tvprox.make_options(iter_hist=hist))
     hn = hist.cpu().numpy()
@@ -527,7 +536,7 @@ def bench_configs(args, ws, rank, local, peak):
             w.X = np.ascontiguousarray(w.X[off:off + per])
             w.grad = np.ascontiguousarray(w.grad[off:off + per])
         barrier(ws)
-        res[name] = time_2d_config(w, dev, ws, 10 if name == "C5" else 20, flush, peak)
+        res[name] = time_2d_config(w, dev, ws, 10 if name == "C5" else 20, flush, peak, cluster=name == "C5")
         res[name]["images_per_rank"] = per
         del w
         torch.cuda.empty_cache()

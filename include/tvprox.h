@@ -67,10 +67,14 @@ typedef enum { TVP_OK = 0, TVP_EINVAL = 1, TVP_EUNSUPPORTED = 2, TVP_ECUDA = 3 }
  * calling thread's fused-2D default (tvp_set_fused2d).
  *
  *   fused2d      2D only.  -1: the calling thread's default (initially on, unless
- *                the environment has TVP_FUSED2D=0); 0: staged row / column passes
- *                through HBM; 1: planes with 32 < H, W <= 64 run all K Dykstra
- *                passes on chip.  The output, saved masks and
- *                gradients are bitwise the same either way.
+ *                the environment has TVP_FUSED2D=0): planes with 32 < H, W <= 64 run
+ *                all K Dykstra passes on chip in one CTA; 0: staged
+ *                row / column passes through HBM; 1: on chip wherever supported,
+ *                i.e. also fp32 planes whose sides are both in 65..128 or both in
+ *                129..224 (C5's 224^2), held by a thread-block cluster of 2-8 CTAs
+ *                (distributed shared memory; measured slower than the staged passes
+ *                at C5 on B200, so only on request or with TVP_FUSED2D=2).  The
+ *                output, saved masks and gradients are bitwise the same either way.
  *   line_search  Globalisation of the projected Newton step:
  *                TVP_LS_BACKTRACK (default) = projected Armijo search with
  *                quadratic-interpolation backtracking ("only iterates a few times",

@@ -1088,6 +1088,7 @@ struct PlaneFwdArgs {
     int ls_after;             // PN iteration from which the projected line search runs (a-7)
     int32_t* diag;            // nullable: accumulated line counters (line_diag)
     int32_t* hist;            // nullable: [2K][kHistBins] (pass 2(k-1) rows, 2(k-1)+1 columns)
+    int coarse;               // cold passes (k = 1) start from the coarse bound set (cluster kernels)
 };
 
 template <typename T, int ER, int EC, int WPB, bool LSP>

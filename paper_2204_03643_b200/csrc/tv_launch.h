@@ -73,6 +73,20 @@ inline cudaError_t launch_plane_fwd(const PlaneFwdArgs<T>& a, cudaStream_t s, bo
 }
 template <typename T> cudaError_t launch_plane_bwd(const PlaneBwdArgs<T>& a, cudaStream_t s);
 inline bool plane_fwd_supported(int64_t H, int64_t W) { return H > 32 && H <= 64 && W > 32 && W <= 64; }
+// f2 on a thread-block cluster (tv_cluster.cuh): fp32 planes whose rows and columns both
+// take the half-warp geometry of the staged passes with the same E (65..128 -> E = 8,
+// 129..224 -> E = 14), so the result is bitwise the staged one.
+inline bool plane_cl_supported(int64_t H, int64_t W, int esz) {
+    if (esz != 4 || !geo16_knob()) return false;
+    const Geo gh = pick_geo(H, 4), gw = pick_geo(W, 4);
+    return gh.LPR == 16 && gw.LPR == 16 && gh.E == gw.E;
+}
+template <typename T, bool LSP> cudaError_t launch_plane_fwd_cl_ls(const PlaneFwdArgs<T>& a, cudaStream_t s);
+template <typename T> cudaError_t launch_plane_bwd_cl(const PlaneBwdArgs<T>& a, cudaStream_t s);
+template <typename T>
+inline cudaError_t launch_plane_fwd_cl(const PlaneFwdArgs<T>& a, cudaStream_t s, bool lsp) {
+    return lsp ? launch_plane_fwd_cl_ls<T, true>(a, s) : launch_plane_fwd_cl_ls<T, false>(a, s);
+}
 template <typename T> cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s);
 template <typename T> cudaError_t launch_col_bwd(ColBwdArgs<T> a, cudaStream_t s);
 template <typename T> cudaError_t launch_lam_reduce(const LamReduceArgs<T>& a, cudaStream_t s);

@@ -4,8 +4,10 @@
 #include <mutex>
 #include <unordered_map>
 #include <cstdlib>
+#include <cstdio>
 
 #include "tv_kernels.cuh"
+#include "tv_cluster.cuh"
 #include "tv_launch.h"
 
 namespace tvp {
@@ -440,6 +442,133 @@ cudaError_t launch_plane_bwd(const PlaneBwdArgs<T>& a, cudaStream_t s) {
     if (ec == 7) return plane_bwd_t<T, 8, 7>(a, s);
     return plane_bwd_t<T, 8, 8>(a, s);
 }
+
+// f2 on a thread-block cluster (tv_cluster.cuh): grid = NC x the clusters that fit the
+// device at once (cudaOccupancyMaxActiveClusters), each cluster looping over planes.
+// The smem opt-in and the cluster occupancy are cached per (device, kernel, smem).
+template <typename K>
+static cudaError_t cluster_grid(K kern, int threads, size_t smem, int nc, int64_t work, int& grid) {
+    static std::mutex mu;
+    static std::unordered_map<OccKey, int, OccKeyHash> cache;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int ncl = 0;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        const OccKey key{dev, reinterpret_cast<const void*>(kern), smem};
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            if (smem > 48 * 1024) {
+                e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+            }
+            if (nc > 8) {
+                e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                if (e != cudaSuccess) return e;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(nc, 1, 1);
+            cfg.blockDim = dim3(threads, 1, 1);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = nc;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+            if (e != cudaSuccess) return e;
+            cache[key] = ncl;
+            if (env_int("TVP_CL_VERBOSE", 0))
+                fprintf(stderr, "[tvp] cluster kernel: %d clusters of %d CTAs x %d threads, %zu B smem\n", ncl, nc,
+                        threads, smem);
+        } else {
+            ncl = it->second;
+        }
+    }
+    if (ncl < 1) return cudaErrorInvalidConfiguration;
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, ncl)) * nc;
+    return cudaSuccess;
+}
+
+template <typename K, typename A>
+static cudaError_t cluster_launch(K kern, const A& a, int grid, int threads, size_t smem, int nc, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = nc;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+    count_launch();
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+// Cluster size per line geometry: TVP_CL_NC14 / TVP_CL_NC8 (A/B knobs) pick 4 or 8 CTAs
+// for the E = 14 planes (129..224) and 2 or 4 for the E = 8 planes (65..128).
+static int cl_nc14() {
+    static const int v = env_int("TVP_CL_NC14", 4) == 8 ? 8 : 4;
+    return v;
+}
+static int cl_nc8() {
+    static const int v = env_int("TVP_CL_NC8", 2) == 4 ? 4 : 2;
+    return v;
+}
+
+template <typename T, int E, int NC, int WPB, bool LSP>
+static cudaError_t plane_fwd_cl_t(PlaneFwdArgs<T> a, cudaStream_t s) {
+    a.coarse = (coarse_knob() && coarse16_knob()) ? 1 : 0;    // as the staged cold passes
+    auto kern = k_plane_fwd_cl<T, E, NC, WPB, LSP>;
+    const size_t smem = cl_smem_bytes<T>(a.H, a.W, NC, WPB, true);
+    int grid = 0;
+    cudaError_t e = cluster_grid(kern, WPB * 32, smem, NC, a.planes, grid);
+    if (e != cudaSuccess) return e;
+    return cluster_launch(kern, a, grid, WPB * 32, smem, NC, s);
+}
+
+template <typename T, bool LSP>
+cudaError_t launch_plane_fwd_cl_ls(const PlaneFwdArgs<T>& a, cudaStream_t s) {
+    if constexpr (sizeof(T) == 4) {
+        if (pick_geo(a.H, 4).E == 14)
+            return cl_nc14() == 8 ? plane_fwd_cl_t<T, 14, 8, 8, LSP>(a, s) : plane_fwd_cl_t<T, 14, 4, 16, LSP>(a, s);
+        return cl_nc8() == 4 ? plane_fwd_cl_t<T, 8, 4, 8, LSP>(a, s) : plane_fwd_cl_t<T, 8, 2, 16, LSP>(a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <typename T, int E, int NC, int WPB>
+static cudaError_t plane_bwd_cl_t(const PlaneBwdArgs<T>& a, cudaStream_t s) {
+    auto kern = k_plane_bwd_cl<T, E, NC, WPB>;
+    const size_t smem = cl_smem_bytes<T>(a.H, a.W, NC, WPB, false);
+    int grid = 0;
+    cudaError_t e = cluster_grid(kern, WPB * 32, smem, NC, a.planes, grid);
+    if (e != cudaSuccess) return e;
+    return cluster_launch(kern, a, grid, WPB * 32, smem, NC, s);
+}
+
+template <typename T>
+cudaError_t launch_plane_bwd_cl(const PlaneBwdArgs<T>& a, cudaStream_t s) {
+    if constexpr (sizeof(T) == 4) {
+        if (pick_geo(a.H, 4).E == 14)
+            return cl_nc14() == 8 ? plane_bwd_cl_t<T, 14, 8, 8>(a, s) : plane_bwd_cl_t<T, 14, 4, 16>(a, s);
+        return cl_nc8() == 4 ? plane_bwd_cl_t<T, 8, 4, 8>(a, s) : plane_bwd_cl_t<T, 8, 2, 16>(a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+#define TVP_INST_CLUSTER(T)                                                                        \
+    template cudaError_t launch_plane_fwd_cl_ls<T, false>(const PlaneFwdArgs<T>&, cudaStream_t);     \
+    template cudaError_t launch_plane_fwd_cl_ls<T, true>(const PlaneFwdArgs<T>&, cudaStream_t);      \
+    template cudaError_t launch_plane_bwd_cl<T>(const PlaneBwdArgs<T>&, cudaStream_t);
 
 // Explicit instantiations, split over several translation units (tv_inst_*.cu) so the
 // build compiles them in parallel.

@@ -25,6 +25,16 @@ static bool fused2d_env() {
     }();
     return v;
 }
+// TVP_FUSED2D=2: the default also takes the thread-block-cluster planes (65..224 per side),
+// which are otherwise only used on explicit request (tvp_options_t.fused2d = 1): on B200
+// they measure slower than the staged passes for C5.
+static bool cluster_env() {
+    static const bool v = [] {
+        const char* e = getenv("TVP_FUSED2D");
+        return e && atoi(e) == 2;
+    }();
+    return v;
+}
 static thread_local int g_fused2d = -1;     // -1: not set on this thread (environment default)
 int geo16_knob() {
     static const int v = [] {
@@ -51,6 +61,7 @@ static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 // Resolved per-call options (tvp_options_t, include/tvprox.h).
 struct Opts {
     bool fused2d;
+    bool cluster;       // f2 also for the thread-block-cluster planes
     bool lsp;
     int ls_after;
     int32_t* diag;
@@ -62,6 +73,7 @@ static bool resolve_opts(const tvp_options_t* o, Opts& r) {
     const int after = o ? o->ls_after : 0;
     if (f < -1 || f > 1 || (ls != TVP_LS_BACKTRACK && ls != TVP_LS_PARALLEL) || after < 0) return false;
     r.fused2d = f == -1 ? (g_fused2d == -1 ? fused2d_env() : g_fused2d != 0) : f != 0;
+    r.cluster = f == 1 || (f == -1 && g_fused2d == -1 && cluster_env());
     r.lsp = ls == TVP_LS_PARALLEL;
     r.ls_after = after == 0 ? kLsAfterDefault : after;
     r.diag = o ? o->diag : nullptr;
@@ -300,8 +312,10 @@ static tvp_status_t tv2d_fwd_impl(const void* Xv, void* Yv, int64_t N, int64_t C
         cudaError_t e = cudaMemsetAsync(line_iters, 0, sizeof(int32_t) * 2 * K, s);
         if (e != cudaSuccess) return cuda_status(e, "tv2d_prox_fwd");
     }
-    if (o.fused2d && plane_fwd_supported(H, W)) {
-        // f2: the whole plane stays on chip for all K passes (no Z/P/Q workspace traffic)
+    const bool cl = o.cluster && plane_cl_supported(H, W, (int)sizeof(T));
+    if ((o.fused2d && plane_fwd_supported(H, W)) || cl) {
+        // f2: the whole plane stays on chip for all K passes (no Z/P/Q workspace traffic):
+        // one CTA per plane up to 64 x 64, a thread-block cluster up to 224 x 224
         PlaneFwdArgs<T> f{};
         f.X = X;
         f.Y = Y;
@@ -320,6 +334,7 @@ static tvp_status_t tv2d_fwd_impl(const void* Xv, void* Yv, int64_t N, int64_t C
         f.ls_after = o.ls_after;
         f.diag = o.diag;
         f.hist = o.hist;
+        if (cl) return cuda_status(launch_plane_fwd_cl<T>(f, s, o.lsp), "tv2d_prox_fwd(fused cluster)");
         return cuda_status(launch_plane_fwd<T>(f, s, o.lsp), "tv2d_prox_fwd(fused)");
     }
     for (int k = 1; k <= K; ++k) {
@@ -415,7 +430,8 @@ static tvp_status_t tv2d_bwd_impl(const void* GYv, const void* saved, void* GXv,
     const T* G = static_cast<const T*>(GYv);
     T* GX = static_cast<T*>(GXv);
     const int64_t HW2 = H + W;
-    const bool fused = o.fused2d && plane_fwd_supported(H, W);
+    const bool cl = o.cluster && plane_cl_supported(H, W, (int)sizeof(T));
+    const bool fused = (o.fused2d && plane_fwd_supported(H, W)) || cl;
     if (fused) {
         // f2: both adjoint planes stay on chip through all 2K adjoint passes
         PlaneBwdArgs<T> f{};
@@ -429,7 +445,7 @@ static tvp_status_t tv2d_bwd_impl(const void* GYv, const void* saved, void* GXv,
         f.mwr = (int)mwr;
         f.mwc = (int)mwc;
         f.lampart = glam ? lampart : nullptr;
-        cudaError_t e = launch_plane_bwd<T>(f, s);
+        cudaError_t e = cl ? launch_plane_bwd_cl<T>(f, s) : launch_plane_bwd<T>(f, s);
         if (e != cudaSuccess) return cuda_status(e, "tv2d_prox_bwd(fused)");
     }
     for (int k = K; k >= 1 && !fused; --k) {

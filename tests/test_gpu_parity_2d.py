@@ -298,7 +298,11 @@ def test_inference_no_saved(tp, H, W):
 
 @pytest.mark.parametrize("H,W,K,mode,dt", [(56, 56, 4, "channel", "f32"), (33, 64, 3, "scalar", "f32"),
                                             (64, 40, 2, "plane", "f32"), (50, 61, 1, "channel", "f32"),
-                                            (56, 56, 4, "channel", "f64"), (64, 64, 5, "scalar", "f32")])
+                                            (56, 56, 4, "channel", "f64"), (64, 64, 5, "scalar", "f32"),
+                                            # thread-block-cluster f2 (65..224 per side, fp32)
+                                            (224, 224, 4, "channel", "f32"), (150, 200, 3, "scalar", "f32"),
+                                            (224, 129, 2, "plane", "f32"), (128, 128, 4, "channel", "f32"),
+                                            (70, 100, 1, "scalar", "f32"), (97, 65, 5, "plane", "f32")])
 def test_fused_plane_matches_staged_bitwise(tp, H, W, K, mode, dt):
     """f2: the on-chip plane kernel gives bitwise the staged passes' output, saved masks
     and iteration counts (same line solver, same lane geometry), and matches the oracle."""
