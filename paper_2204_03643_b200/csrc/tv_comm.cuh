@@ -15,6 +15,7 @@ constexpr int kCommSlots = 16;
 
 template <typename T, int LPR, int WPL>
 struct Comm {
+    static constexpr bool kCluster = false;
     int l;      // lane within the warp group [0, LPR)
     int w;      // warp within the line [0, WPL)
     T* sv;      // [kCommSlots][3][WPL]   (WPL > 1)

@@ -157,11 +157,11 @@ __device__ __forceinline__ void smem_to_regs(const T* buf, int l, T (&y)[E]) {
 // Solve one line held by this lane group: centring, pinning, non-finite
 // detection, PN solve.  Writes the uncentred output into `w` and returns the
 // status (row_iters code).
-template <typename T, int E, int LPR, int WPL, bool PE, bool LSP = false>
+template <typename T, int E, int LPR, int WPL, bool PE, bool LSP = false, typename CM = Comm<T, LPR, WPL>>
 __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& lam, int n,
                                           bool valid, uint32_t warm_pos, uint32_t warm_neg,
-                                          const Comm<T, LPR, WPL>& C, bool coarse = false,
-                                          T* xb = nullptr, int ls_after = kLsAfterDefault) {
+                                          const CM& C, bool coarse = false,
+                                          T* xb = nullptr, int ls_after = kLsAfterDefault, int max_iters = 0) {
     const int ll = C.w * LPR + C.l;           // line lane
     constexpr uint32_t allm = (E == 32) ? 0xffffffffu : ((1u << (E & 31)) - 1u);
     uint32_t pin;
@@ -204,16 +204,19 @@ __device__ __forceinline__ int solve_line(T (&y)[E], T (&w)[E], Lam<T, E, PE>& l
     for (int k = 0; k < E; ++k) y[k] -= mean;
     // cold solve: initial bound set from the block-restricted problem (coarse_init);
     // lines held by a full warp or more (short lines converge in 3-5 iterations cold)
-    if (!PE && LPR * WPL >= TVP_COARSE_MINLANES && WPL <= TVP_COARSE_MAXWPL && (sizeof(T) == 4 || WPL <= 2) && coarse &&
-        n / E >= 3) {
-        uint32_t cp, cn;
-        coarse_init<T, E, LPR, WPL>(y, lam.r, n, active, C, xb, cp, cn);
-        warm_pos |= cp;
-        warm_neg |= cn;
+    if constexpr (!CM::kCluster) {
+        if (!PE && LPR * WPL >= TVP_COARSE_MINLANES && WPL <= TVP_COARSE_MAXWPL && (sizeof(T) == 4 || WPL <= 2) &&
+            coarse && n / E >= 3) {
+            uint32_t cp, cn;
+            coarse_init<T, E, LPR, WPL>(y, lam.r, n, active, C, xb, cp, cn);
+            warm_pos |= cp;
+            warm_neg |= cn;
+        }
     }
     T u[E];
     int lsp = 0;
-    int st = pn_solve<T, E, LPR, WPL, PE, LSP>(y, u, w, pin, warm_pos, warm_neg, lam, C, active, ls_after, lsp);
+    int st = pn_solve<T, E, LPR, WPL, PE, LSP>(y, u, w, pin, warm_pos, warm_neg, lam, C, active, ls_after, lsp,
+                                               max_iters);
 #pragma unroll
     for (int k = 0; k < E; ++k) w[k] = active ? w[k] + mean : (bad ? nan_<T>() : y[k]);
     if (!active) st = bad ? -2 : 0;

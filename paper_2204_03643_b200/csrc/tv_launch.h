@@ -38,9 +38,10 @@ inline Geo pick_geo(int64_t n, int esz = 8) {
     return {32, 32};
 }
 constexpr int64_t kMaxLine = 1024;                 // 2D lines (W, H)
-// 1D rows: a CTA of up to 16 warps holds the row in registers (E = 16 fp32, 8 fp64)
-constexpr int64_t kMaxLine1DF32 = 16 * 32 * 16;    // 8192
-constexpr int64_t kMaxLine1DF64 = 8 * 32 * 16;     // 4096
+// 1D rows: a CTA of up to 16 warps holds the row in registers (E = 16 fp32, 8 fp64), up
+// to 8192 / 4096 samples; beyond, a thread-block cluster of up to 16 such CTAs (f4).
+constexpr int64_t kMaxLine1DF32 = 16 * 16 * 32 * 16;    // 131072
+constexpr int64_t kMaxLine1DF64 = 16 * 16 * 32 * 8;     // 65536
 // First-level chunks of the lambda-gradient reduction: a function of the sizes only
 // (never of the GPU), so results are bitwise reproducible across devices.
 inline int lam_chunks(int64_t total, int64_t nout) {

@@ -8,6 +8,7 @@
 
 #include "tv_kernels.cuh"
 #include "tv_cluster.cuh"
+#include "tv_long.cuh"
 #include "tv_launch.h"
 
 namespace tvp {
@@ -224,9 +225,15 @@ cudaError_t row_fwd_prepass(RowFwdArgs<T>& a, bool per_edge, bool dykstra, cudaS
     return cudaSuccess;
 }
 
+// f4 beyond one CTA: a thread-block cluster per row (tv_long.cuh), defined below.
+constexpr int64_t long_row_per_cta(int esz) { return esz == 4 ? 16 * 32 * 16 : 16 * 32 * 8; }
+template <typename T, bool LSP> cudaError_t launch_row_fwd_long(const RowFwdArgs<T>& a, bool per_edge, cudaStream_t s);
+template <typename T> cudaError_t launch_row_bwd_long(const RowBwdArgs<T>& a, bool per_edge, cudaStream_t s);
+
 template <typename T, bool LSP>
 cudaError_t launch_row_fwd_ls(RowFwdArgs<T> a, bool per_edge, bool dykstra, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
+    if (a.n > long_row_per_cta((int)sizeof(T))) return launch_row_fwd_long<T, LSP>(a, per_edge, s);
     if (a.n > 1024) {
         // long 1D rows (f4): one CTA of WPL warps holds the row in registers, E = 16
         // (fp32) / 8 (fp64) samples per lane; in-kernel coarse solve
@@ -309,6 +316,7 @@ static cudaError_t row_bwd_w_t(const RowBwdArgs<T>& a, cudaStream_t s) {
 template <typename T>
 cudaError_t launch_row_bwd(const RowBwdArgs<T>& a, bool dykstra, bool per_edge, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
+    if (a.n > long_row_per_cta((int)sizeof(T))) return launch_row_bwd_long<T>(a, per_edge, s);
     if (a.n > 1024) {                             // long 1D rows (f4): one CTA of WPL warps per row
         if constexpr (sizeof(T) == 4) {
             if (a.n <= 2048) return per_edge ? row_bwd_w_t<T, 16, 4, false, true>(a, s) : row_bwd_w_t<T, 16, 4, false, false>(a, s);
@@ -564,6 +572,55 @@ cudaError_t launch_plane_bwd_cl(const PlaneBwdArgs<T>& a, cudaStream_t s) {
     }
     return cudaErrorInvalidValue;
 }
+
+// f4: a cluster of NCTA = 2..16 CTAs (the smallest power of two that holds the row), each
+// CTA 16 warps x 32 lanes x E samples in registers (E = 16 fp32, 8 fp64).
+static int long_ncta(int64_t n, int esz) {
+    const int64_t per = long_row_per_cta(esz);
+    const int64_t c = (n + per - 1) / per;
+    return c <= 2 ? 2 : (c <= 4 ? 4 : (c <= 8 ? 8 : 16));
+}
+template <typename T, int NCTA, bool PE, bool LSP>
+static cudaError_t row_fwd_cl_t(const RowFwdArgs<T>& a, cudaStream_t s) {
+    constexpr int E = sizeof(T) == 4 ? 16 : 8, WPL = 16;
+    auto kern = k_row_fwd_cl<T, E, WPL, NCTA, PE, LSP>;
+    const size_t smem = long_comm_bytes<T>(WPL * NCTA, WPL);
+    int grid = 0;
+    cudaError_t e = cluster_grid(kern, WPL * 32, smem, NCTA, a.nlines, grid);
+    if (e != cudaSuccess) return e;
+    return cluster_launch(kern, a, grid, WPL * 32, smem, NCTA, s);
+}
+template <typename T, bool LSP>
+cudaError_t launch_row_fwd_long(const RowFwdArgs<T>& a, bool per_edge, cudaStream_t s) {
+    switch (long_ncta(a.n, (int)sizeof(T))) {
+        case 2: return per_edge ? row_fwd_cl_t<T, 2, true, LSP>(a, s) : row_fwd_cl_t<T, 2, false, LSP>(a, s);
+        case 4: return per_edge ? row_fwd_cl_t<T, 4, true, LSP>(a, s) : row_fwd_cl_t<T, 4, false, LSP>(a, s);
+        case 8: return per_edge ? row_fwd_cl_t<T, 8, true, LSP>(a, s) : row_fwd_cl_t<T, 8, false, LSP>(a, s);
+        default: return per_edge ? row_fwd_cl_t<T, 16, true, LSP>(a, s) : row_fwd_cl_t<T, 16, false, LSP>(a, s);
+    }
+}
+template <typename T, int NCTA, bool PE>
+static cudaError_t row_bwd_cl_t(const RowBwdArgs<T>& a, cudaStream_t s) {
+    constexpr int E = sizeof(T) == 4 ? 16 : 8, WPL = 16;
+    auto kern = k_row_bwd_cl<T, E, WPL, NCTA, PE>;
+    const size_t smem = long_comm_bytes<T>(WPL * NCTA);
+    int grid = 0;
+    cudaError_t e = cluster_grid(kern, WPL * 32, smem, NCTA, a.nlines, grid);
+    if (e != cudaSuccess) return e;
+    return cluster_launch(kern, a, grid, WPL * 32, smem, NCTA, s);
+}
+template <typename T>
+cudaError_t launch_row_bwd_long(const RowBwdArgs<T>& a, bool per_edge, cudaStream_t s) {
+    switch (long_ncta(a.n, (int)sizeof(T))) {
+        case 2: return per_edge ? row_bwd_cl_t<T, 2, true>(a, s) : row_bwd_cl_t<T, 2, false>(a, s);
+        case 4: return per_edge ? row_bwd_cl_t<T, 4, true>(a, s) : row_bwd_cl_t<T, 4, false>(a, s);
+        case 8: return per_edge ? row_bwd_cl_t<T, 8, true>(a, s) : row_bwd_cl_t<T, 8, false>(a, s);
+        default: return per_edge ? row_bwd_cl_t<T, 16, true>(a, s) : row_bwd_cl_t<T, 16, false>(a, s);
+    }
+}
+#define TVP_INST_LONG_FWD(T, LSP) \
+    template cudaError_t launch_row_fwd_long<T, LSP>(const RowFwdArgs<T>&, bool, cudaStream_t);
+#define TVP_INST_LONG_BWD(T) template cudaError_t launch_row_bwd_long<T>(const RowBwdArgs<T>&, bool, cudaStream_t);
 
 #define TVP_INST_CLUSTER(T)                                                                        \
     template cudaError_t launch_plane_fwd_cl_ls<T, false>(const PlaneFwdArgs<T>&, cudaStream_t);     \

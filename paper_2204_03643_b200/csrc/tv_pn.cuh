@@ -263,11 +263,11 @@ template <> __device__ __forceinline__ double big_<double>() { return 1.0e300; }
 // of the line (slack bound).  Returns the line status: iterations (| 1<<16 if
 // accepted at a stall), or -1 (max iterations, w = x(u)).
 // ---------------------------------------------------------------------------
-template <typename T, int E, int LPR, int WPL, bool PE, bool LSP = false>
+template <typename T, int E, int LPR, int WPL, bool PE, bool LSP = false, typename CM = Comm<T, LPR, WPL>>
 __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], uint32_t pin,
                                         uint32_t warm_pos, uint32_t warm_neg,
-                                        const Lam<T, E, PE>& lam, const Comm<T, LPR, WPL>& C,
-                                        bool active, int ls_after, int& ls_passes) {
+                                        const Lam<T, E, PE>& lam, const CM& C,
+                                        bool active, int ls_after, int& ls_passes, int max_iters = 0) {
     warm_pos &= ~pin;
     warm_neg &= ~pin;
 #pragma unroll
@@ -281,7 +281,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
     const T eps = Num<T>::eps;
     const T slackA = eps * T(8);     // summation-error slack of the KKT test (x sum |terms|)
     const T slack1 = T(1) + T(2) * eps;
-    const int maxit = Num<T>::max_iters;
+    const int maxit = max_iters > 0 ? max_iters : Num<T>::max_iters;
 
     bool run = active, first = true, fin = false, uchg = true, fin_direct = false;
     bool conv = false, stall = false;
@@ -646,9 +646,9 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
 //             every warp solves the whole coarse line redundantly (WPL samples
 //             per lane, warp shuffles only); jump bits come back by ballots.
 // ---------------------------------------------------------------------------
-template <typename T, int E, int LPR, int WPL>
+template <typename T, int E, int LPR, int WPL, typename CM = Comm<T, LPR, WPL>>
 __device__ __forceinline__ void coarse_init(const T (&y)[E], T lam_r, int n, bool active,
-                                            const Comm<T, LPR, WPL>& C, T* xb,
+                                            const CM& C, T* xb,
                                             uint32_t& cpos, uint32_t& cneg) {
     const int ll = C.w * LPR + C.l;
     const int nc = n / E;
@@ -709,9 +709,9 @@ __device__ __forceinline__ void coarse_init(const T (&y)[E], T lam_r, int n, boo
 // mean_right(e)) = sum_seg (s_R - s_L) mean_seg (dx/dlam = (s_R - s_L)/len).
 // Comm slots 0..2 are used.
 // ---------------------------------------------------------------------------
-template <typename T, int E, int LPR, int WPL>
+template <typename T, int E, int LPR, int WPL, typename CM = Comm<T, LPR, WPL>>
 __device__ __forceinline__ void seg_mean_c(T (&v)[E], uint32_t bnd, uint32_t pos, uint32_t neg,
-                                           const Comm<T, LPR, WPL>& C, T& lam_part) {
+                                           const CM& C, T& lam_part) {
     // pass 1: means of the segments that end inside the lane; the lane's first
     // segment keeps its partial sum (it still lacks the carry), the open tail sum
     // goes to the scan

@@ -172,8 +172,45 @@ def test_forward_inference_no_mask(tp, n):
     assert np.abs(x - x_ref).max() <= TOL["f32"] * rng_range(y.astype(np.float64))
 
 
+@pytest.mark.parametrize("n,nrows", [(8193, 5), (12000, 4), (16384, 4), (30000, 3), (48000, 3), (65536, 2),
+                                     (100000, 2), (131072, 2)])
+def test_forward_cluster_rows_fp32(tp, n, nrows):
+    """f4 past one CTA: a thread-block cluster of 2-16 CTAs holds the row in registers."""
+    y = workloads.random_rows(9900 + n, nrows, n, "step", np.float32)
+    lam = np.random.default_rng(n + 9).uniform(0.05, 2.0, nrows).astype(np.float32)
+    x, mask, it = run_gpu(tp, y, lam, torch.float32)
+    check_forward(y, lam.astype(np.float64), x, mask, it, "f32")
+
+
+@pytest.mark.parametrize("n", [4097, 10000, 32768, 65536])
+def test_forward_cluster_rows_fp64(tp, n):
+    y = workloads.random_rows(9950 + n, 2, n, "normal", np.float64)
+    lam = np.random.default_rng(n + 10).uniform(0.05, 2.0, 2)
+    x, mask, it = run_gpu(tp, y, lam, torch.float64)
+    check_forward(y, lam, x, mask, it, "f64")
+
+
+@pytest.mark.parametrize("n", [16384, 48000, 100000])
+def test_backward_cluster_rows(tp, n):
+    y = workloads.random_rows(9960 + n, 3, n, "step", np.float32)
+    lam = np.random.default_rng(n + 11).uniform(0.05, 1.0, 3).astype(np.float32)
+    _bwd_compare(tp, y, lam, 1, torch.float32, "f32", n)
+
+
+@pytest.mark.parametrize("n", [20000])
+def test_per_edge_lambda_cluster_rows(tp, n):
+    rng = np.random.default_rng(9970 + n)
+    y = rng.standard_normal((2, n)).astype(np.float32)
+    lam = rng.uniform(0.0, 1.2, (2, n - 1)).astype(np.float32)
+    lam[rng.random(lam.shape) < 0.1] = 0.0
+    _bwd_compare(tp, y, lam, 2, torch.float32, "f32", n)
+
+
 def test_long_row_limit(tp):
-    y = torch.zeros((2, 8193), device="cuda")
+    from paper_2204_03643_b200 import _lib
+    lib = _lib.load()
+    assert lib.tvp_max_line_1d(_lib.TVP_F32) == 131072 and lib.tvp_max_line_1d(_lib.TVP_F64) == 65536
+    y = torch.zeros((2, 131073), device="cuda")
     with pytest.raises(Exception):
         tp.tv1d_fwd(y, 0.5)
 
