@@ -636,12 +636,14 @@ def cpu_baseline(seconds=10.0, rows_per_batch=4096):
 
     done, el = run(cores, seconds, rows_per_batch)
     d1, e1 = run(1, 3.0, 512)
-    w5 = workloads.c5(N=16)
-    P = 48
-    t0 = time.perf_counter()
+    n5 = 128
+    w5 = workloads.c5(N=n5)
+    P = 3 * n5
     Xp = w5.X.reshape(P, 224, 224).astype(np.float64)
-    Yr, segs = oracle.prox2d_batch(Xp, np.tile(w5.lam, 16), 4, nthreads=cores)
-    oracle.bwd2d_batch(segs, w5.grad.reshape(P, 224, 224).astype(np.float64), 4, nthreads=cores)
+    G5 = w5.grad.reshape(P, 224, 224).astype(np.float64)
+    t0 = time.perf_counter()
+    Yr, segs = oracle.prox2d_batch(Xp, np.tile(w5.lam, n5), 4, nthreads=cores)
+    oracle.bwd2d_batch(segs, G5, 4, nthreads=cores)
     e5 = time.perf_counter() - t0
     return {"value": done / el, "unit": "rows/s", "cores": cores, "kind": "oracle",
             "sample": "%d C2 rows (1024 samples, per-row lambda) fwd+bwd in %.1f s, fp64 C oracle, %d threads"
@@ -650,7 +652,7 @@ def cpu_baseline(seconds=10.0, rows_per_batch=4096):
             "single_thread": {"value": d1 / e1, "unit": "rows/s", "cores": 1,
                               "sample": "%d C2 rows fwd+bwd in %.1f s, 1 thread" % (d1, e1)},
             "c5_2d": {"value": P * 224 * 224 / e5 / 1e6, "unit": "Mpixel/s", "cores": cores,
-                      "sample": "16 C5 images (48 planes of 224^2, K = 4) fwd + reverse mode in %.1f s" % e5}}
+                      "sample": "%d C5 images (%d planes of 224^2, K = 4) fwd + reverse mode in %.1f s" % (n5, P, e5)}}
 
 
 def issue_roofline(warp_instr, ms, peaks):

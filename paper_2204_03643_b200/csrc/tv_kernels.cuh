@@ -134,6 +134,55 @@ __device__ __forceinline__ void st_contig(T* __restrict__ p, int i0, int n, bool
     }
 }
 
+// Lane-contiguous I/O straight between HBM and registers (the register-direct row
+// kernels): lane l's E samples [i0, i0 + E) of one line, as 16-byte vectors (vw >= 4,
+// E % 4 == 0), 8-byte vectors (vw >= 2, E even) or scalars; samples past n read as 0.
+// vw = the widest vector every line start of the call is aligned to (row_vw).
+template <typename T, int E>
+__device__ __forceinline__ void ld_lane(const T* __restrict__ p, int i0, int n, int vw, T (&v)[E]) {
+    if (sizeof(T) == 4 && (E % 4) == 0 && vw >= 4 && i0 + E <= n) {
+#pragma unroll
+        for (int q = 0; q < E / 4; ++q) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(p + i0) + q);
+            v[4 * q] = (T)f.x; v[4 * q + 1] = (T)f.y; v[4 * q + 2] = (T)f.z; v[4 * q + 3] = (T)f.w;
+        }
+    } else if (sizeof(T) == 4 && (E % 2) == 0 && vw >= 2 && i0 + E <= n) {
+#pragma unroll
+        for (int q = 0; q < E / 2; ++q) {
+            const float2 f = __ldg(reinterpret_cast<const float2*>(p + i0) + q);
+            v[2 * q] = (T)f.x; v[2 * q + 1] = (T)f.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = (i0 + k < n) ? __ldg(p + i0 + k) : T(0);
+    }
+}
+template <typename T, int E>
+__device__ __forceinline__ void st_lane(T* __restrict__ p, int i0, int n, int vw, const T (&v)[E]) {
+    if (sizeof(T) == 4 && (E % 4) == 0 && vw >= 4 && i0 + E <= n) {
+#pragma unroll
+        for (int q = 0; q < E / 4; ++q)
+            reinterpret_cast<float4*>(p + i0)[q] = make_float4((float)v[4 * q], (float)v[4 * q + 1],
+                                                              (float)v[4 * q + 2], (float)v[4 * q + 3]);
+    } else if (sizeof(T) == 4 && (E % 2) == 0 && vw >= 2 && i0 + E <= n) {
+#pragma unroll
+        for (int q = 0; q < E / 2; ++q)
+            reinterpret_cast<float2*>(p + i0)[q] = make_float2((float)v[2 * q], (float)v[2 * q + 1]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+            if (i0 + k < n) p[i0 + k] = v[k];
+    }
+}
+// Widest vector (elements, 4 / 2 / 1) that every line start base + r * stride is aligned to.
+template <typename T>
+__device__ __forceinline__ int row_vw(int64_t stride, uintptr_t bases) {
+    if (sizeof(T) != 4) return 1;
+    if ((stride & 3) == 0 && (bases & 15) == 0) return 4;
+    if ((stride & 1) == 0 && (bases & 7) == 0) return 2;
+    return 1;
+}
+
 // Odd pitch of one staged line in shared memory (conflict-free lane reads).
 template <int E, int LPR>
 __host__ __device__ constexpr int line_pitch() {
@@ -411,6 +460,117 @@ k_row_fwd(RowFwdArgs<T> a) {
 }
 
 // ===========================================================================
+// Row forward, register-direct (default for lines of <= 512 samples): G = 32 / LPR lines
+// per warp; every lane loads its E contiguous samples straight from HBM into registers
+// (8- / 16-byte vectors when aligned) and stores its outputs the same way, so a line
+// costs a few vector loads and stores instead of the shared-memory staging round trips
+// of k_row_fwd (whose executed instructions outside the PN loop were ~30 % of a warm
+// 2D pass).  The sectors a warp touches per instruction are reused from L1 by the
+// following instructions, so HBM traffic is the same.  Same solve_line, same result.
+// ===========================================================================
+template <typename T, int E, int LPR, bool PE, bool DYK, int WPB, bool LSP>
+__global__ void __launch_bounds__(WPB * 32, (row_minb<T, E>()))
+k_row_fwd_r(RowFwdArgs<T> a) {
+    constexpr int G = 32 / LPR;
+    __shared__ uint32_t mwb_s[WPB * 32];                 // per warp: G lines x (32 / G) mask words
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / LPR, l = lane % LPR;
+    uint32_t* mwb = mwb_s + warp * 32 + grp * (32 / G);
+    const int n = a.n, i0 = l * E;
+    const int vw = row_vw<T>(a.stride, reinterpret_cast<uintptr_t>(a.src0) | reinterpret_cast<uintptr_t>(a.dst0) |
+                                           reinterpret_cast<uintptr_t>(DYK && a.src1 ? a.src1 : a.src0) |
+                                           reinterpret_cast<uintptr_t>(DYK && a.dst1 ? a.dst1 : a.dst0) |
+                                           reinterpret_cast<uintptr_t>(PE ? a.lam : a.src0));
+    const int64_t ngroups = (a.nlines + G - 1) / G;
+    for (int64_t gi = (int64_t)blockIdx.x * WPB + warp; gi < ngroups; gi += (int64_t)gridDim.x * WPB) {
+        const int64_t r = gi * G + grp;
+        const bool valid = r < a.nlines;
+        const int64_t rr = valid ? r : 0;
+        const int nv = valid ? n : 0;                     // an invalid line loads zeros
+        T y[E], w[E];
+        ld_lane<T, E>(a.src0 + rr * a.stride, i0, nv, vw, y);
+        T akeep[DYK ? E : 1];
+        if (DYK) {
+            // A = Y + P (P = 0 at k = 1: Y + 0, as the staged and fused passes)
+            T pv[E];
+            if (a.src1) ld_lane<T, E>(a.src1 + rr * a.stride, i0, nv, vw, pv);
+            else {
+#pragma unroll
+                for (int k = 0; k < E; ++k) pv[k] = T(0);
+            }
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                y[k] = y[k] + pv[k];
+                akeep[DYK ? k : 0] = y[k];
+            }
+        }
+        Lam<T, E, PE> lam;
+        if (PE) {
+            T le[E];
+            ld_lane<T, E>(a.lam + rr * a.stride, i0, valid ? n - 1 : 0, vw, le);
+#pragma unroll
+            for (int k = 0; k < E; ++k) lam.e[PE ? k : 0] = le[k];
+            lam.r = T(0);
+        } else {
+            lam.r = valid ? line_lambda(a.lam, a.lam_mode, a.lam_scalar, r, a.lines_per_plane, a.C) : T(0);
+        }
+        uint32_t wp = 0, wn = 0;
+        if (a.mask_in && valid && a.mw > 0) {
+            uint32_t wb;
+            mask_window<E>(a.mask_in + r * a.mw, a.mw, i0, wb, wp, wn);
+        }
+        const Comm<T, LPR, 1> C{l, 0, nullptr, nullptr};
+        const int st = solve_line<T, E, LPR, 1, PE, LSP>(y, w, lam, n, valid, wp, wn, C, a.coarse != 0, nullptr,
+                                                         a.ls_after);
+        if (valid) {
+            st_lane<T, E>(a.dst0 + r * a.stride, i0, n, vw, w);
+            if (DYK && a.dst1) {
+                T pv[E];
+#pragma unroll
+                for (int k = 0; k < E; ++k) pv[k] = akeep[DYK ? k : 0] - w[k];
+                st_lane<T, E>(a.dst1 + r * a.stride, i0, n, vw, pv);
+            }
+        }
+        // a-8 mask: each lane codes its E edges from registers; the (at most two) partial
+        // words it touches are OR-ed into the line's word buffer (n <= 512: <= 32 words)
+        if (a.mask_out) {
+            mwb[l] = 0u;                                  // 32 / G == LPR words per line
+            const T wnx = shdn<LPR>(w[0], 1);
+            const int wlo = i0 >> 4;
+            uint32_t clo = 0u, chi = 0u;
+            if constexpr (E <= 16 && !PE) {
+                const uint32_t code = lane_codes<T, E>(w, wnx, i0, n - 1, !(lam.r > T(0)));
+                const int sh = 2 * (i0 & 15);
+                clo = code << sh;
+                chi = sh ? (code >> (32 - sh)) : 0u;
+            } else {
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    const int e = i0 + k;
+                    const T xr = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : wnx;
+                    const bool lz = PE ? !(lam.e[PE ? k : 0] > T(0)) : !(lam.r > T(0));
+                    const uint32_t code = (e < n - 1) ? edge_code(w[k], xr, lz) << (2 * (e & 15)) : 0u;
+                    if ((e >> 4) == wlo) clo |= code; else chi |= code;
+                }
+            }
+            __syncwarp();
+            if (valid && clo) atomicOr(&mwb[wlo], clo);
+            if (valid && chi) atomicOr(&mwb[wlo + 1], chi);
+            __syncwarp();
+            if (valid) {
+                for (int q = l; q < a.mw; q += LPR) a.mask_out[r * a.mw + q] = mwb[q];
+            }
+            __syncwarp();
+        }
+        if (valid && l == 0) {
+            if (a.row_iters) a.row_iters[r] = st;
+            if (a.iters_max) atomicMax(a.iters_max, st >= 0 ? (st & 0xffff) : (1 << 20));
+            line_diag(st, a.diag, a.hist);
+        }
+    }
+}
+
+// ===========================================================================
 // Row forward with WPL warps per line (E samples per lane, 32*WPL lanes per line):
 // the block is one line at a time; cross-warp scans through shared memory.
 // ===========================================================================
@@ -681,6 +841,82 @@ __global__ void __launch_bounds__(WPB * 32) k_coarse_rows2(RowFwdArgs<T> a) {
     }
 }
 
+// 16-byte-vector staging of a full [H x TC] column tile (fp32, TC % 4 == 0, rows aligned).
+template <typename T, int TC>
+__device__ __forceinline__ bool tile_v4(int W, int tcw, uintptr_t ptrs) {
+    return sizeof(T) == 4 && (TC % 4) == 0 && tcw == TC && (W & 3) == 0 && (ptrs & 15) == 0;
+}
+// Load: t0 = S0[h][c], t1 = S1[h][c] (0 if S1 null) for the tile; d0[c*LP + spad(h)] =
+// t0 + sgn * t1 (sgn = +1: Z + Q; -1: A - B) and, if d1, d1[...] = t1.  Each thread moves
+// 4 columns of a row per step (one float4 per plane), transposing into the lines.
+template <int TC, int LP>
+__device__ __forceinline__ void tile_ld4(const float* __restrict__ S0, const float* __restrict__ S1, int H, int W,
+                                         float sgn, float* d0, float* d1, int nth) {
+    constexpr int C4 = TC / 4, U = 4;
+    for (int i0 = threadIdx.x; i0 < H * C4; i0 += nth * U) {
+        float4 a0[U], a1[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int idx = i0 + q * nth;
+            const int h = idx / C4, c4 = idx - h * C4;
+            const bool in = idx < H * C4;
+            const int64_t off = (int64_t)h * W + 4 * c4;
+            a0[q] = in ? __ldg(reinterpret_cast<const float4*>(S0 + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            a1[q] = (in && S1) ? __ldg(reinterpret_cast<const float4*>(S1 + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int idx = i0 + q * nth;
+            if (idx < H * C4) {
+                const int h = idx / C4, c = 4 * (idx - h * C4);
+                const int sh = spad(h);
+                if (sgn > 0.f) {
+                    d0[(c + 0) * LP + sh] = a0[q].x + a1[q].x;
+                    d0[(c + 1) * LP + sh] = a0[q].y + a1[q].y;
+                    d0[(c + 2) * LP + sh] = a0[q].z + a1[q].z;
+                    d0[(c + 3) * LP + sh] = a0[q].w + a1[q].w;
+                } else {
+                    d0[(c + 0) * LP + sh] = a0[q].x - a1[q].x;
+                    d0[(c + 1) * LP + sh] = a0[q].y - a1[q].y;
+                    d0[(c + 2) * LP + sh] = a0[q].z - a1[q].z;
+                    d0[(c + 3) * LP + sh] = a0[q].w - a1[q].w;
+                }
+                if (d1) {
+                    d1[(c + 0) * LP + sh] = a1[q].x;
+                    d1[(c + 1) * LP + sh] = a1[q].y;
+                    d1[(c + 2) * LP + sh] = a1[q].z;
+                    d1[(c + 3) * LP + sh] = a1[q].w;
+                }
+            }
+        }
+    }
+}
+// Store: O0[h][c] = x = s0[c*LP + spad(h)]; if O1: O1[h][c] = s1[...] - x (sgn < 0, the
+// Dykstra correction) -- or, with O1 null and sgn > 0, O0 = s0 + s1 (the adjoint update).
+template <int TC, int LP>
+__device__ __forceinline__ void tile_st4(float* __restrict__ O0, float* __restrict__ O1, int H, int W,
+                                         const float* s0, const float* s1, float sgn, int nth) {
+    constexpr int C4 = TC / 4;
+    for (int idx = threadIdx.x; idx < H * C4; idx += nth) {
+        const int h = idx / C4, c = 4 * (idx - h * C4);
+        const int sh = spad(h);
+        const int64_t off = (int64_t)h * W + c;
+        float4 x = make_float4(s0[(c + 0) * LP + sh], s0[(c + 1) * LP + sh], s0[(c + 2) * LP + sh], s0[(c + 3) * LP + sh]);
+        if (sgn > 0.f) {
+            x.x = x.x + s1[(c + 0) * LP + sh];
+            x.y = x.y + s1[(c + 1) * LP + sh];
+            x.z = x.z + s1[(c + 2) * LP + sh];
+            x.w = x.w + s1[(c + 3) * LP + sh];
+        }
+        *reinterpret_cast<float4*>(O0 + off) = x;
+        if (O1) {
+            const float4 q = make_float4(s1[(c + 0) * LP + sh] - x.x, s1[(c + 1) * LP + sh] - x.y,
+                                         s1[(c + 2) * LP + sh] - x.z, s1[(c + 3) * LP + sh] - x.w);
+            *reinterpret_cast<float4*>(O1 + off) = q;
+        }
+    }
+}
+
 // ===========================================================================
 // Column forward: Dykstra column pass (tile of TC columns of one plane).
 // ===========================================================================
@@ -707,6 +943,12 @@ k_col_fwd(ColFwdArgs<T> a) {
         const int tcw = min(TC, W - c0);
         const int64_t base = p * HW + c0;
         // ---- coalesced load of the [H x TC] tile, transposed into line-major smem
+        // (16-byte vectors of 4 columns when the tile is full and rows are aligned)
+        if (tile_v4<T, TC>(W, tcw, reinterpret_cast<uintptr_t>(a.Z) | reinterpret_cast<uintptr_t>(a.Q ? a.Q : a.Z))) {
+            tile_ld4<TC, LP>(reinterpret_cast<const float*>(a.Z) + base,
+                             a.Q ? reinterpret_cast<const float*>(a.Q) + base : nullptr, H, W, 1.f,
+                             reinterpret_cast<float*>(bufA), nullptr, nth);
+        } else {
         constexpr int U = 8;
         for (int i0 = threadIdx.x; i0 < H * TC; i0 += nth * U) {
             T v0[U], v1[U];
@@ -724,6 +966,7 @@ k_col_fwd(ColFwdArgs<T> a) {
                 const int h = idx / TC, c = idx - h * TC;
                 if (idx < H * TC) bufA[c * LP + spad(h)] = v0[q] + v1[q];
             }
+        }
         }
         for (int idx = threadIdx.x; idx < (LPR * E - H) * TC; idx += nth) {
             int h = H + idx / TC, c = idx % TC;
@@ -791,6 +1034,10 @@ k_col_fwd(ColFwdArgs<T> a) {
             }
         }
         __syncthreads();
+        if (tile_v4<T, TC>(W, tcw, reinterpret_cast<uintptr_t>(a.Y) | reinterpret_cast<uintptr_t>(a.Qout ? a.Qout : a.Y))) {
+            tile_st4<TC, LP>(reinterpret_cast<float*>(a.Y) + base, a.Qout ? reinterpret_cast<float*>(a.Qout) + base : nullptr,
+                             H, W, reinterpret_cast<const float*>(bufX), reinterpret_cast<const float*>(bufA), -1.f, nth);
+        } else {
         for (int idx = threadIdx.x; idx < H * TC; idx += nth) {
             int h = idx / TC, c = idx - h * TC;
             if (c < tcw) {
@@ -798,6 +1045,7 @@ k_col_fwd(ColFwdArgs<T> a) {
                 a.Y[base + (int64_t)h * W + c] = xv;
                 if (a.Qout) a.Qout[base + (int64_t)h * W + c] = bufA[c * LP + spad(h)] - xv;
             }
+        }
         }
         __syncthreads();
     }
@@ -913,6 +1161,70 @@ k_row_bwd(RowBwdArgs<T> a) {
 }
 
 // ===========================================================================
+// Row backward, register-direct (default for lines of <= 256 samples): G = 32 / LPR
+// lines per warp, lane-contiguous vector loads and stores (see k_row_fwd_r).
+// ===========================================================================
+template <typename T, int E, int LPR, bool DYK, bool PE, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+k_row_bwd_r(RowBwdArgs<T> a) {
+    constexpr int G = 32 / LPR;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / LPR, l = lane % LPR;
+    const int n = a.n, i0 = l * E;
+    const int vw = row_vw<T>(a.stride, reinterpret_cast<uintptr_t>(a.out) |
+                                           reinterpret_cast<uintptr_t>(DYK ? a.B : a.A) |
+                                           reinterpret_cast<uintptr_t>(DYK && a.A ? a.A : a.out));
+    const int64_t ngroups = (a.nlines + G - 1) / G;
+    for (int64_t gi = (int64_t)blockIdx.x * WPB + warp; gi < ngroups; gi += (int64_t)gridDim.x * WPB) {
+        const int64_t r = gi * G + grp;
+        const bool valid = r < a.nlines;
+        const int64_t rr = valid ? r : 0;
+        const int nv = valid ? n : 0;
+        T v[E], pb[E];
+        if (DYK) {
+            // r = B - Pbar (Pbar = A, or 0 at k = K); A <- Pbar + rowsegmean(r)
+            ld_lane<T, E>(a.B + rr * a.stride, i0, nv, vw, v);
+            if (a.A) ld_lane<T, E>(a.A + rr * a.stride, i0, nv, vw, pb);
+            else {
+#pragma unroll
+                for (int k = 0; k < E; ++k) pb[k] = T(0);
+            }
+#pragma unroll
+            for (int k = 0; k < E; ++k) v[k] = v[k] - pb[k];
+        } else {
+            ld_lane<T, E>(a.A + rr * a.stride, i0, nv, vw, v);
+        }
+        uint32_t bnd, pos, neg;
+        bwd_mask_bits<E>(a.mask + rr * a.mw, a.mw, n, l, bnd, pos, neg);
+        T lp = T(0);
+        seg_mean<T, E, LPR>(v, bnd, pos, neg, l, lp);
+        if (PE) {
+            const T vn = shdn<LPR>(v[0], 1);
+            if (a.lam_edge && valid) {
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    const int e = i0 + k;
+                    const T nxt = (k + 1 < E) ? v[(k + 1 < E) ? k + 1 : k] : vn;
+                    if (e < n - 1) {
+                        const T sg = ((pos >> k) & 1u) ? T(1) : (((neg >> k) & 1u) ? T(-1) : T(0));
+                        a.lam_edge[r * a.stride + e] = sg * (v[k] - nxt);
+                    }
+                }
+            }
+        }
+        lp = group_sum<LPR>(lp);
+        if (valid && l == 0 && a.lam_line) a.lam_line[(r / a.lam_lpp) * a.lam_pstride + (r % a.lam_lpp)] = lp;
+        if (valid) {
+            if (DYK) {
+#pragma unroll
+                for (int k = 0; k < E; ++k) v[k] = pb[k] + v[k];
+            }
+            st_lane<T, E>(a.out + r * a.stride, i0, n, vw, v);
+        }
+    }
+}
+
+// ===========================================================================
 // Row backward, one line per block of 32*WPL threads (long lines): each thread
 // holds E contiguous samples loaded straight from HBM into registers (16-byte
 // vector loads when aligned), segment mean through the Comm group, 16-byte
@@ -1015,6 +1327,12 @@ k_col_bwd(ColBwdArgs<T> a) {
         const int c0 = (int)(tile % tpp) * TC;
         const int tcw = min(TC, W - c0);
         const int64_t base = p * HW + c0;
+        if (tile_v4<T, TC>(W, tcw, reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.B ? a.B : a.A)) &&
+            LPR * E == H) {
+            tile_ld4<TC, LP>(reinterpret_cast<const float*>(a.A) + base,
+                             a.B ? reinterpret_cast<const float*>(a.B) + base : nullptr, H, W, -1.f,
+                             reinterpret_cast<float*>(bufV), reinterpret_cast<float*>(bufB), nth);
+        } else {
         constexpr int U = 8;
         for (int i0 = threadIdx.x; i0 < LPR * E * TC; i0 += nth * U) {
             T va[U], vb[U];
@@ -1035,6 +1353,7 @@ k_col_bwd(ColBwdArgs<T> a) {
                     bufB[c * LP + spad(h)] = vb[q];
                 }
             }
+        }
         }
         __syncthreads();
         for (int cg = warp; cg < TC / G; cg += WPB) {
@@ -1057,9 +1376,14 @@ k_col_bwd(ColBwdArgs<T> a) {
             }
         }
         __syncthreads();
+        if (tile_v4<T, TC>(W, tcw, reinterpret_cast<uintptr_t>(a.Bout))) {
+            tile_st4<TC, LP>(reinterpret_cast<float*>(a.Bout) + base, nullptr, H, W,
+                             reinterpret_cast<const float*>(bufB), reinterpret_cast<const float*>(bufV), 1.f, nth);
+        } else {
         for (int idx = threadIdx.x; idx < H * TC; idx += nth) {
             int h = idx / TC, c = idx - h * TC;
             if (c < tcw) a.Bout[base + (int64_t)h * W + c] = bufB[c * LP + spad(h)] + bufV[c * LP + spad(h)];
+        }
         }
         __syncthreads();
     }
@@ -1094,8 +1418,12 @@ struct PlaneFwdArgs {
     int coarse;               // cold passes (k = 1) start from the coarse bound set (cluster kernels)
 };
 
+#ifndef TVP_PLANE_DYN
+#define TVP_PLANE_DYN 1
+#endif
 template <typename T, int ER, int EC, int WPB, bool LSP>
-__global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) : 1)) k_plane_fwd(PlaneFwdArgs<T> a) {
+__global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? (512 / (WPB * 32) > 0 ? 512 / (WPB * 32) : 1) : 1))
+k_plane_fwd(PlaneFwdArgs<T> a) {
     constexpr int LPR = 8, G = 4;                     // 8 lanes per line, 4 lines per warp
     extern __shared__ __align__(16) unsigned char smraw_[];
     const int H = a.H, W = a.W, K = a.K;
@@ -1115,6 +1443,21 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
     const int64_t HW = (int64_t)H * W;
     const int64_t rset = a.planes * H * a.mwr, cset = a.planes * W * a.mwc;
     const Comm<T, LPR, 1> Cm{l, 0, nullptr, nullptr};
+    // line groups are handed to warps by a shared counter per orientation (TVP_PLANE_DYN=0:
+    // static round robin); PN iteration counts vary per line and each pass ends at a barrier
+    __shared__ int s_next[2];
+    if (threadIdx.x == 0) s_next[0] = s_next[1] = 0;
+    auto next_task = [&](int o, int t) -> int {
+#if TVP_PLANE_DYN
+        (void)t;
+        int v = 0;
+        if (lane == 0) v = atomicAdd(&s_next[o], 1);
+        return __shfl_sync(FULL, v, 0);
+#else
+        (void)o;
+        return t + WPB;
+#endif
+    };
     for (int64_t p = blockIdx.x; p < a.planes; p += gridDim.x) {
         const T lamp = line_lambda(a.lam, a.lam_mode, a.lam_scalar, p, 1, a.C);
         const bool lz = !(lamp > T(0));
@@ -1125,8 +1468,9 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
         __syncthreads();
         for (int k = 1; k <= K; ++k) {
             // ---------------- row pass: Z = rowprox(Y + P); P <- (Y + P) - Z
+            if (threadIdx.x == 0) s_next[1] = 0;
 #pragma unroll 1
-            for (int t = warp; t * G < H; t += WPB) {
+            for (int t = TVP_PLANE_DYN ? next_task(0, 0) : warp; t * G < H; t = next_task(0, t)) {
                 const int r = t * G + grp;
                 const bool valid = r < H;
                 const uint32_t wp0 = k > 1 ? wrp[t * 32 + lane] : 0u, wn0 = k > 1 ? wrn[t * 32 + lane] : 0u;
@@ -1179,8 +1523,9 @@ __global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? 512 / (WPB * 32) :
             }
             __syncthreads();
             // ---------------- column pass: Y = colprox(Z + Q); Q <- (Z + Q) - Y
+            if (threadIdx.x == 0) s_next[0] = 0;
 #pragma unroll 1
-            for (int t = warp; t * G < W; t += WPB) {
+            for (int t = TVP_PLANE_DYN ? next_task(1, 0) : warp; t * G < W; t = next_task(1, t)) {
                 const int c = t * G + grp;
                 const bool valid = c < W;
                 const uint32_t wp0 = k > 1 ? wcp[t * 32 + lane] : 0u, wn0 = k > 1 ? wcn[t * 32 + lane] : 0u;

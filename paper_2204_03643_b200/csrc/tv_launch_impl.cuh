@@ -130,10 +130,27 @@ static bool coarse16_knob() {
     return v;
 }
 
+// TVP_ROW_DIRECT=0 (A/B): rows of <= 512 samples staged through shared memory (k_row_fwd /
+// k_row_bwd) instead of the register-direct kernels (k_row_fwd_r / k_row_bwd_r).
+static bool row_direct_knob() {
+    static const bool v = env_int("TVP_ROW_DIRECT", 1) != 0;
+    return v;
+}
+
 template <typename T, int E, int LPR, bool PE, bool DYK, bool LSP>
 static cudaError_t row_fwd_t(RowFwdArgs<T> a, cudaStream_t s) {
     constexpr int G = 32 / LPR;
     if (LPR < 32 && !coarse16_knob()) a.coarse = 0;
+    if (row_direct_knob()) {
+        auto kern = k_row_fwd_r<T, E, LPR, PE, DYK, kRowWPB, LSP>;
+        const int64_t groups = (a.nlines + G - 1) / G;
+        int grid = 0;
+        cudaError_t e = persistent_grid(kern, kRowWPB * 32, 0, (groups + kRowWPB - 1) / kRowWPB, grid);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kRowWPB * 32, 0, s>>>(a);
+        count_launch();
+        return cudaGetLastError();
+    }
     constexpr int LP = line_pitch<E, LPR>();
     const size_t smem = (size_t)kRowWPB * (DYK ? 2 : 1) * G * LP * sizeof(T) + (size_t)kRowWPB * 32 * 4;
     auto kern = k_row_fwd<T, E, LPR, PE, DYK, kRowWPB, LSP>;
@@ -290,6 +307,16 @@ cudaError_t launch_col_fwd_ls(ColFwdArgs<T> a, cudaStream_t s) {
 template <typename T, int E, int LPR, bool DYK, bool PE>
 static cudaError_t row_bwd_t(const RowBwdArgs<T>& a, cudaStream_t s) {
     constexpr int G = 32 / LPR;
+    if (row_direct_knob()) {
+        auto kern = k_row_bwd_r<T, E, LPR, DYK, PE, kRowWPB>;
+        const int64_t groups = (a.nlines + G - 1) / G;
+        int grid = 0;
+        cudaError_t e = persistent_grid(kern, kRowWPB * 32, 0, (groups + kRowWPB - 1) / kRowWPB, grid);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kRowWPB * 32, 0, s>>>(a);
+        count_launch();
+        return cudaGetLastError();
+    }
     constexpr int LP = line_pitch<E, LPR>();
     const size_t smem = (size_t)kRowWPB * (DYK ? 2 : 1) * G * LP * sizeof(T);
     auto kern = k_row_bwd<T, E, LPR, DYK, PE, kRowWPB>;

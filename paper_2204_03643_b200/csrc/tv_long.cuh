@@ -28,7 +28,7 @@ __host__ __device__ constexpr size_t long_comm_bytes(int NW, int WPL = 0) {
 // Iteration cap of the cluster-wide solve (the default 64 / 100 is for lines of one CTA:
 // rows of 16K-131K samples measured p90 20-28, max 52-54 PN iterations from the
 // domain-decomposition start, tools/diag_long.py).
-constexpr int kLongMaxIters = 256;
+constexpr int kLongMaxIters = 128;
 
 template <typename T, int E, int WPL, int NCTA, bool PE, bool LSP>
 __global__ void __launch_bounds__(WPL * 32, 1) k_row_fwd_cl(RowFwdArgs<T> a) {

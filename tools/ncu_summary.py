@@ -115,7 +115,12 @@ def main():
         lines.append("")
     with open(os.path.join(prof, "%s_ncu_summary.md" % tag), "w") as f:
         f.write("\n".join(lines) + "\n")
-    tj = {}
+    tjp = os.path.join(prof, "ncu_traffic.json")
+    try:
+        with open(tjp) as f:
+            tj = json.load(f)            # merge: a capture set without C2 keeps the C2 keys
+    except Exception:
+        tj = {}
     for name, pipes in pipe_info.items():
         if name.endswith("c2_row_fwd"):
             tj["c2_fwd_pipes"] = pipes
@@ -125,15 +130,23 @@ def main():
     wi = {n: v for n, v in warp_instr.items() if n.endswith(("c2_row_fwd", "c2_coarse"))}
     if wi:
         tj["c2_fwd_warp_instr_per_launch"] = sum(wi.values())
+    byk = {}
     for k, v in traffic.items():
         if k.endswith("c2_row_fwd"):
             tj["c2_fwd_bytes_per_launch"] = v
+            byk["k_row_fwd_w (fine projected Newton)"] = v
+        elif k.endswith("c2_coarse"):
+            byk["k_coarse_rows2 (coarse pre-pass)"] = v
         elif k.endswith("c2_row_bwd"):
             tj["c2_bwd_bytes_per_launch"] = v
         else:
             tj[k] = v
-    tj["source"] = "profiles/%s_ncu_summary.md (ncu --set full, one launch each)" % tag
-    with open(os.path.join(prof, "ncu_traffic.json"), "w") as f:
+    if byk:
+        # DRAM bytes of EVERY kernel of the C2 forward op (roofline.traffic in bench.py)
+        tj["c2_fwd_bytes_by_kernel"] = byk
+        tj["c2_fwd_op_bytes_per_launch"] = sum(byk.values())
+        tj["source"] = "profiles/%s_ncu_summary.md (ncu --set full, one launch each)" % tag
+    with open(tjp, "w") as f:
         json.dump(tj, f, indent=1)
     # launch list
     ll = glob.glob(os.path.join(src, "launches_%s.csv" % tag))
