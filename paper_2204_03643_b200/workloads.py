@@ -129,6 +129,21 @@ def t1(reading="a", with_grad=True) -> Workload1D:
     return Workload1D("T1" + reading, y, np.ones(b), "scalar", 1.0, "f32", seed, g)
 
 
+def long_rows(n, batch=None, with_grad=True) -> Workload1D:
+    """f4 ("long 1D signals", BJ:5): C2's generator at length n -- unit step at n/2 plus
+    N(0, sigma^2), sigma 0.1 / 0.5 alternating -- with per-row lambda softplus(U(-2, 1))
+    scaled by sqrt(n / 1024) (the noise TV grows with sqrt(n)); 2^26 samples per batch."""
+    b = batch or max(1, (1 << 26) // n)
+    seed = 1000 * 7 + n
+    rng = np.random.default_rng(seed)
+    y = np.zeros((b, n))
+    y[:, n // 2:] = 1.0
+    y += rng.standard_normal((b, n)) * np.where(np.arange(b) % 2 == 0, 0.1, 0.5)[:, None]
+    lam = softplus_np(np.random.default_rng(seed + 1).uniform(-2.0, 1.0, b)) * np.sqrt(n / 1024.0)
+    g = np.random.default_rng(seed + 2).standard_normal((b, n)).astype(np.float32) if with_grad else None
+    return Workload1D("L%d" % n, y.astype(np.float32), lam, "row", 0.0, "f32", seed, g)
+
+
 def c3(N=64, C=64, H=56, W=56, with_grad=True) -> Workload2D:
     seed = 1000 * 3
     rng = np.random.default_rng(seed + 0)
