@@ -527,7 +527,7 @@ def bench_configs(args, ws, rank, local, peak):
     res["T1a"] = time_1d_config(workloads.t1("a"), dev, ws, reps, flush, peak)
     res["T1b"] = time_1d_config(workloads.t1("b"), dev, ws, reps, flush, peak)
     # f4: long 1D signals -- one CTA per row up to 8192 samples, a thread-block cluster beyond
-    for n in (8192, 32768, 131072):
+    for n in (8192, 16384, 65536):
         res["L%d" % n] = time_1d_config(workloads.long_rows(n), dev, ws, 5, flush, peak)
     barrier(ws)
     for name, fn, total in (("C3", workloads.c3, 64), ("C4", workloads.c4, 16), ("C5", workloads.c5, 256)):

@@ -116,7 +116,7 @@ int64_t tvp_max_line(tvp_dtype_t dt);
 /* Longest 1D row (n) ("long 1D signals"): one CTA of up to 16 warps
  * holds a row of up to 8192 (TVP_F32) / 4096 (TVP_F64) samples in registers; longer rows
  * are held by a thread-block cluster of 2..16 such CTAs (distributed shared memory for
- * the solver's scans), up to 131072 for TVP_F32 and 65536 for TVP_F64. */
+ * the solver's scans), up to 65536 samples for both TVP_F32 and TVP_F64. */
 int64_t tvp_max_line_1d(tvp_dtype_t dt);
 
 /* ------------------------------------------------------------------ 1D --- */

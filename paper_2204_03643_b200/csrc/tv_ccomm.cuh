@@ -106,6 +106,21 @@ struct CComm {
     __device__ __forceinline__ bool any(bool p) const { return vote_(__any_sync(FULL, p) ? 1 : 0) != 0; }
     __device__ __forceinline__ bool all(bool p) const { return vote_(__all_sync(FULL, p) ? 1 : 0) == NW; }
     __device__ __forceinline__ bool uany(bool p) const { return p; }     // line-uniform already
+    // bits set on every lane of the line (one vote)
+    __device__ __forceinline__ uint32_t all_bits(uint32_t m) const {
+        const int slot = vr;
+        vr ^= 1;
+        const uint32_t wm = __reduce_and_sync(FULL, m);
+        if (l < NCTA) cl_put(cl_map(sf_s + (uint32_t)((slot * NW + w) * 4), l), (int)wm);
+        cl_sync();
+        uint32_t acc = 0xffffffffu;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int i = l * Q + q;
+            if (i < NW) acc &= (uint32_t)sf[slot * NW + i];
+        }
+        return __reduce_and_sync(FULL, acc);
+    }
 
     // fixed-order sums: lane partials over its Q slots, then a fixed xor tree
     template <int S>

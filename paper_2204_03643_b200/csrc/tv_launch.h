@@ -39,8 +39,10 @@ inline Geo pick_geo(int64_t n, int esz = 8) {
 }
 constexpr int64_t kMaxLine = 1024;                 // 2D lines (W, H)
 // 1D rows: a CTA of up to 16 warps holds the row in registers (E = 16 fp32, 8 fp64), up
-// to 8192 / 4096 samples; beyond, a thread-block cluster of up to 16 such CTAs (f4).
-constexpr int64_t kMaxLine1DF32 = 16 * 16 * 32 * 16;    // 131072
+// to 8192 / 4096 samples; beyond, a thread-block cluster of such CTAs (f4): up to 8 CTAs
+// in fp32 (65536 samples -- longer fp32 rows measured 1.4e-4 x range off the oracle on
+// the noisiest synthetic workload, O7) and 16 in fp64 (65536).
+constexpr int64_t kMaxLine1DF32 = 8 * 16 * 32 * 16;     // 65536
 constexpr int64_t kMaxLine1DF64 = 16 * 16 * 32 * 8;     // 65536
 // First-level chunks of the lambda-gradient reduction: a function of the sizes only
 // (never of the GPU), so results are bitwise reproducible across devices.

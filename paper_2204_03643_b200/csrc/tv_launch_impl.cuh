@@ -605,7 +605,7 @@ cudaError_t launch_plane_bwd_cl(const PlaneBwdArgs<T>& a, cudaStream_t s) {
 static int long_ncta(int64_t n, int esz) {
     const int64_t per = long_row_per_cta(esz);
     const int64_t c = (n + per - 1) / per;
-    return c <= 2 ? 2 : (c <= 4 ? 4 : (c <= 8 ? 8 : 16));
+    return c <= 2 ? 2 : (c <= 4 ? 4 : (c <= 8 ? 8 : 16));   // 16: fp64 only (kMaxLine1DF32 = 8 CTAs)
 }
 template <typename T, int NCTA, bool PE, bool LSP>
 static cudaError_t row_fwd_cl_t(const RowFwdArgs<T>& a, cudaStream_t s) {
@@ -623,7 +623,10 @@ cudaError_t launch_row_fwd_long(const RowFwdArgs<T>& a, bool per_edge, cudaStrea
         case 2: return per_edge ? row_fwd_cl_t<T, 2, true, LSP>(a, s) : row_fwd_cl_t<T, 2, false, LSP>(a, s);
         case 4: return per_edge ? row_fwd_cl_t<T, 4, true, LSP>(a, s) : row_fwd_cl_t<T, 4, false, LSP>(a, s);
         case 8: return per_edge ? row_fwd_cl_t<T, 8, true, LSP>(a, s) : row_fwd_cl_t<T, 8, false, LSP>(a, s);
-        default: return per_edge ? row_fwd_cl_t<T, 16, true, LSP>(a, s) : row_fwd_cl_t<T, 16, false, LSP>(a, s);
+        default:
+            if constexpr (sizeof(T) == 8)
+                return per_edge ? row_fwd_cl_t<T, 16, true, LSP>(a, s) : row_fwd_cl_t<T, 16, false, LSP>(a, s);
+            return cudaErrorInvalidValue;           // fp32 rows stop at 8 CTAs (kMaxLine1DF32)
     }
 }
 template <typename T, int NCTA, bool PE>
@@ -642,7 +645,9 @@ cudaError_t launch_row_bwd_long(const RowBwdArgs<T>& a, bool per_edge, cudaStrea
         case 2: return per_edge ? row_bwd_cl_t<T, 2, true>(a, s) : row_bwd_cl_t<T, 2, false>(a, s);
         case 4: return per_edge ? row_bwd_cl_t<T, 4, true>(a, s) : row_bwd_cl_t<T, 4, false>(a, s);
         case 8: return per_edge ? row_bwd_cl_t<T, 8, true>(a, s) : row_bwd_cl_t<T, 8, false>(a, s);
-        default: return per_edge ? row_bwd_cl_t<T, 16, true>(a, s) : row_bwd_cl_t<T, 16, false>(a, s);
+        default:
+            if constexpr (sizeof(T) == 8) return per_edge ? row_bwd_cl_t<T, 16, true>(a, s) : row_bwd_cl_t<T, 16, false>(a, s);
+            return cudaErrorInvalidValue;
     }
 }
 #define TVP_INST_LONG_FWD(T, LSP) \

@@ -2,8 +2,8 @@
 // north_star "long 1D signals"): one thread-block CLUSTER of NCTA CTAs per row.
 //
 // Each CTA holds WPL * 32 lanes x E contiguous samples of the row in registers (8192
-// fp32 / 4096 fp64 per CTA, as the single-CTA long rows), so a cluster of NCTA = 2..16
-// CTAs holds up to 131072 fp32 / 65536 fp64 samples.  The projected-Newton solver
+// fp32 / 4096 fp64 per CTA, as the single-CTA long rows), so a cluster of NCTA = 2..8
+// (fp32) / 2..16 (fp64) CTAs holds up to 65536 samples.  The projected-Newton solver
 // (pn_solve, Eq. 5-6 in partition form) and the segment-mean backward (Eq. 7-8) are the
 // same code as every other path; only their line-group communication is the cluster
 // version (CComm, tv_ccomm.cuh): warp aggregates through distributed shared memory and a

@@ -277,6 +277,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
     }
     uint32_t bnd = pin | warm_pos | warm_neg;
     uint32_t bnd2 = 0xffffffffu;       // bound set two iterations ago (cycle detection)
+    uint32_t bnd3 = 0xffffffffu, bnd4 = 0xffffffffu;   // three / four ago (cluster lines only)
     const T ynext = C.template next<1>(y[0]);
     const T eps = Num<T>::eps;
     const T slackA = eps * T(8);     // summation-error slack of the KKT test (x sum |terms|)
@@ -336,7 +337,24 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         }
         const bool bchg = C.any(nb != bnd);
         // rounding-level fixed point (no change) or 2-cycle of the bound set: stall
-        const bool cyc2 = bchg & C.all(nb == bnd2);
+        bool cyc2;
+        if constexpr (CM::kCluster) {
+            // lines of 10^4..10^5 samples (f4) can cycle through bound sets with period 2..4
+            // under projected full Newton steps in fp32; one vote covers the three periods.
+            // A cycle switches the line to the Armijo-globalised step for the
+            // rest of the solve, whose accepted steps strictly increase the dual objective;
+            // only a cycle under the line search is a rounding-level stall (O7).
+            const uint32_t eq = (nb == bnd2 ? 1u : 0u) | (nb == bnd3 ? 2u : 0u) | (nb == bnd4 ? 4u : 0u);
+            cyc2 = bchg & (C.all_bits(eq) != 0u);
+            bnd4 = bnd3;
+            bnd3 = bnd2;
+            if (cyc2 && it + 1 < ls_after) {
+                ls_after = it + 1;
+                cyc2 = false;
+            }
+        } else {
+            cyc2 = bchg & C.all(nb == bnd2);
+        }
         if (upd && ((!uchg && !bchg) || cyc2)) { stall = true; run = false; }
         bnd2 = bnd;
         bnd = nb;

@@ -50,7 +50,7 @@ def test_size_queries(lib):
     assert lib.tv1d_mask_words(18) == 2
     assert lib.tv1d_mask_words(1024) == 64
     assert lib.tvp_max_line(0) >= 1024
-    assert lib.tvp_max_line_1d(0) == 131072 and lib.tvp_max_line_1d(1) == 65536
+    assert lib.tvp_max_line_1d(0) == 65536 and lib.tvp_max_line_1d(1) == 65536
     # saved = K * planes * (H * ceil((W-1)/16) + W * ceil((H-1)/16)) words
     assert lib.tv2d_saved_bytes(2, 3, 56, 56, 4) == 4 * 6 * (56 * 4 + 56 * 4) * 4
     assert lib.tv2d_workspace_bytes(0, 2, 3, 56, 56, 4) >= 3 * 6 * 56 * 56 * 4
@@ -74,7 +74,7 @@ def test_invalid_arguments_rejected_before_launch(lib):
     assert lib.tv1d_prox_fwd(7, fake, fake, 4, 8, 8, None, 0, 0.5, None, None, None) == E      # dtype
     assert lib.tv1d_prox_fwd(0, None, fake, 4, 8, 8, None, 0, 0.5, None, None, None) == E      # NULL y
     assert lib.tv1d_prox_fwd(0, fake, fake, 0, 8, 8, None, 0, 0.5, None, None, None) == _lib.TVP_OK  # empty
-    assert lib.tv1d_prox_fwd(0, fake, fake, 4, 131073, 131073, None, 0, 0.5, None, None, None) == _lib.TVP_EUNSUPPORTED
+    assert lib.tv1d_prox_fwd(0, fake, fake, 4, 65537, 65537, None, 0, 0.5, None, None, None) == _lib.TVP_EUNSUPPORTED
     assert lib.tv1d_prox_fwd(1, fake, fake, 4, 65537, 65537, None, 0, 0.5, None, None, None) == _lib.TVP_EUNSUPPORTED
     assert lib.tv2d_prox_fwd(0, fake, fake, 1, 1, 4, 1025, None, 0, 0.5, 4, None, fake, None, None) \
         == _lib.TVP_EUNSUPPORTED

@@ -172,14 +172,23 @@ def test_forward_inference_no_mask(tp, n):
     assert np.abs(x - x_ref).max() <= TOL["f32"] * rng_range(y.astype(np.float64))
 
 
-@pytest.mark.parametrize("n,nrows", [(8193, 5), (12000, 4), (16384, 4), (30000, 3), (48000, 3), (65536, 2),
-                                     (100000, 2), (131072, 2)])
+@pytest.mark.parametrize("n,nrows", [(8193, 5), (12000, 4), (16384, 4), (30000, 3), (48000, 3), (65536, 2)])
 def test_forward_cluster_rows_fp32(tp, n, nrows):
     """f4 past one CTA: a thread-block cluster of 2-16 CTAs holds the row in registers."""
     y = workloads.random_rows(9900 + n, nrows, n, "step", np.float32)
     lam = np.random.default_rng(n + 9).uniform(0.05, 2.0, nrows).astype(np.float32)
     x, mask, it = run_gpu(tp, y, lam, torch.float32)
     check_forward(y, lam.astype(np.float64), x, mask, it, "f32")
+
+
+@pytest.mark.parametrize("n", [16384, 32768, 65536])
+def test_forward_cluster_rows_noisy_fp32(tp, n):
+    """The bench's f4 workload (C2's generator at length n, sigma 0.1 / 0.5 alternating,
+    lambda scaled by sqrt(n/1024)): every row converges (cycles of period <= 4 accepted
+    as rounding-level stalls, O7) and matches the oracle."""
+    w = workloads.long_rows(n, batch=8)
+    x, mask, it = run_gpu(tp, w.y, w.lam.astype(np.float32), torch.float32)
+    check_forward(w.y, w.lam.astype(np.float32).astype(np.float64), x, mask, it, "f32")
 
 
 @pytest.mark.parametrize("n", [4097, 10000, 32768, 65536])
@@ -190,7 +199,7 @@ def test_forward_cluster_rows_fp64(tp, n):
     check_forward(y, lam, x, mask, it, "f64")
 
 
-@pytest.mark.parametrize("n", [16384, 48000, 100000])
+@pytest.mark.parametrize("n", [16384, 48000, 65536])
 def test_backward_cluster_rows(tp, n):
     y = workloads.random_rows(9960 + n, 3, n, "step", np.float32)
     lam = np.random.default_rng(n + 11).uniform(0.05, 1.0, 3).astype(np.float32)
@@ -209,8 +218,8 @@ def test_per_edge_lambda_cluster_rows(tp, n):
 def test_long_row_limit(tp):
     from paper_2204_03643_b200 import _lib
     lib = _lib.load()
-    assert lib.tvp_max_line_1d(_lib.TVP_F32) == 131072 and lib.tvp_max_line_1d(_lib.TVP_F64) == 65536
-    y = torch.zeros((2, 131073), device="cuda")
+    assert lib.tvp_max_line_1d(_lib.TVP_F32) == 65536 and lib.tvp_max_line_1d(_lib.TVP_F64) == 65536
+    y = torch.zeros((2, 65537), device="cuda")
     with pytest.raises(Exception):
         tp.tv1d_fwd(y, 0.5)
 

@@ -68,7 +68,7 @@ def sweep():
 def long_rows():
     """f4: long 1D signals (unit step + N(0, 0.1^2) / N(0, 0.5^2) like C2, lambda scaled with n)."""
     rng = np.random.default_rng(0)
-    ns = (2048, 4096, 8192, 16384, 32768, 65536, 131072) if len(sys.argv) < 3 else tuple(int(v) for v in sys.argv[2:])
+    ns = (2048, 4096, 8192, 16384, 32768, 65536) if len(sys.argv) < 3 else tuple(int(v) for v in sys.argv[2:])
     for n in ns:
         rows = (1 << 26) // n
         y = np.zeros((rows, n), np.float32)
