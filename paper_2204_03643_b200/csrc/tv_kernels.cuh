@@ -1421,8 +1421,12 @@ struct PlaneFwdArgs {
 #ifndef TVP_PLANE_DYN
 #define TVP_PLANE_DYN 1
 #endif
+// Resident CTAs per SM of the fused plane forward (register cap; TVP_PLANE_MINB for A/B).
+#ifndef TVP_PLANE_MINB
+#define TVP_PLANE_MINB 3
+#endif
 template <typename T, int ER, int EC, int WPB, bool LSP>
-__global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? (512 / (WPB * 32) > 0 ? 512 / (WPB * 32) : 1) : 1))
+__global__ void __launch_bounds__(WPB * 32, (sizeof(T) == 4 ? TVP_PLANE_MINB : 1))
 k_plane_fwd(PlaneFwdArgs<T> a) {
     constexpr int LPR = 8, G = 4;                     // 8 lanes per line, 4 lines per warp
     extern __shared__ __align__(16) unsigned char smraw_[];
