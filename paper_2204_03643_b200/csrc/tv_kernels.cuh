@@ -1306,8 +1306,14 @@ k_row_bwd_w(RowBwdArgs<T> a) {
 // ===========================================================================
 // Column backward: B <- B + colsegmean(A - B)  (Dykstra column adjoint).
 // ===========================================================================
+// Resident CTAs per SM of the E = 14 column adjoint (C5; a register cap: 128 -> 80, the
+// pass is latency-bound; TVP_COLB_MINB for A/B: 4 / 6 / 8 gave C5 bwd 0.990 / 0.974 /
+// 0.981 ms).  Other geometries keep their natural allocation (C4 measured slower capped).
+#ifndef TVP_COLB_MINB
+#define TVP_COLB_MINB 6
+#endif
 template <typename T, int E, int LPR, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
+__global__ void __launch_bounds__(WPB * 32, ((sizeof(T) == 4 && E == 14) ? TVP_COLB_MINB * 4 / WPB : 1))
 k_col_bwd(ColBwdArgs<T> a) {
     constexpr int G = 32 / LPR;
     constexpr int LP = line_pitch<E, LPR>();
@@ -1327,6 +1333,17 @@ k_col_bwd(ColBwdArgs<T> a) {
         const int c0 = (int)(tile % tpp) * TC;
         const int tcw = min(TC, W - c0);
         const int64_t base = p * HW + c0;
+        // the mask words of the warp's first column pair are loaded with the tile, so their
+        // latency overlaps the tile's (the adjoint passes are latency-bound)
+        MaskWin<E> mpre;
+        {
+            const int cp = warp * G + grp;
+            if (cp < tcw && a.mw > 0) mask_words_ld<E>(a.mask + (p * W + c0 + cp) * a.mw, a.mw, l * E, mpre);
+            else {
+#pragma unroll
+                for (int j = 0; j <= MaskWin<E>::NS; ++j) mpre.w[j] = 0u;
+            }
+        }
         if (tile_v4<T, TC>(W, tcw, reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.B ? a.B : a.A)) &&
             LPR * E == H) {
             tile_ld4<TC, LP>(reinterpret_cast<const float*>(a.A) + base,
@@ -1361,8 +1378,13 @@ k_col_bwd(ColBwdArgs<T> a) {
             const bool valid = c < tcw;
             T v[E];
             smem_to_regs<T, E>(bufV + c * LP, l, v);
-            uint32_t bnd, pos, neg;
-            bwd_mask_bits<E>(a.mask + (valid ? (p * W + c0 + c) : 0) * a.mw, a.mw, H, l, bnd, pos, neg);
+            uint32_t bnd = 0, pos = 0, neg = 0;
+            if (cg == warp) {
+                if (a.mw > 0) mask_decode<E>(mpre, l * E, bnd, pos, neg);
+                bnd |= pin_tail<E>(H - 1 - l * E);
+            } else {
+                bwd_mask_bits<E>(a.mask + (valid ? (p * W + c0 + c) : 0) * a.mw, a.mw, H, l, bnd, pos, neg);
+            }
             T lp = T(0);
             seg_mean<T, E, LPR>(v, bnd, pos, neg, l, lp);
             lp = group_sum<LPR>(lp);

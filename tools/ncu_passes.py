@@ -38,10 +38,11 @@ def main():
             pass
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peak = float(json.load(f)["hbm_gbs"])
-    N, C, H, W, K = 256, 3, 224, 224, 4
+    cfg = sys.argv[3] if len(sys.argv) > 3 else "C5"
+    N, C, H, W, K = {"C5": (256, 3, 224, 224, 4), "C4": (16, 3, 512, 512, 4), "C3": (64, 64, 56, 56, 4)}[cfg]
     px = N * C * H * W
-    fwd = [d for d in launches.values() if "k_row_fwd<" in d["kernel"] or "k_col_fwd<" in d["kernel"]]
-    bwd = [d for d in launches.values() if "k_row_bwd<" in d["kernel"] or "k_col_bwd<" in d["kernel"]]
+    fwd = [d for d in launches.values() if any(k in d["kernel"] for k in ("k_row_fwd<", "k_row_fwd_r<", "k_col_fwd<"))]
+    bwd = [d for d in launches.values() if any(k in d["kernel"] for k in ("k_row_bwd<", "k_row_bwd_r<", "k_row_bwd_w<", "k_col_bwd<"))]
     out = []
     for j, d in enumerate(fwd[:2 * K]):
         k, col = j // 2 + 1, j % 2 == 1
@@ -65,18 +66,19 @@ def main():
         table.append("| %s | %s | %.1f | %.1f | %.0f | %.3f | %.2f | %.3f | %.3g | %.1f |" % (
             direction, name, e["us"], byt / 1e6, gbs, e["frac_of_peak"], req, e["required_frac_of_peak"] or 0,
             e["warp_instr"] or 0, e["issue_active_pct"] or 0))
-    doc = {"config": "C5 256x3x224x224 fp32, K=4, staged passes (default path)", "peak_GBps": peak,
-           "source": "profiles/%s_passes_c5.md (ncu --metrics, --clock-control none, one fwd + one bwd)" % tag,
+    doc = {"config": "%s %dx%dx%dx%d fp32, K=%d, staged passes (default path)" % (cfg, N, C, H, W, K),
+           "peak_GBps": peak,
+           "source": "profiles/%s_passes_%s.md (ncu --metrics, --clock-control none, one fwd + one bwd)" % (tag, cfg.lower()),
            "passes": js}
-    with open(os.path.join(ROOT, "profiles", "ncu_passes_c5.json"), "w") as f:
+    with open(os.path.join(ROOT, "profiles", "ncu_passes_%s.json" % cfg.lower()), "w") as f:
         json.dump(doc, f, indent=1)
-    md = ["# Per-pass R2 roofline, C5 (%s)" % tag, "",
+    md = ["# Per-pass R2 roofline, %s (%s)" % (cfg, tag), "",
           "ncu `gpu__time_duration`, `dram__bytes_read/write`, `smsp__inst_executed`, issue active, one launch per "
           "pass (cold L2, serialised).  Peak %.0f GB/s (MEASURED_PEAKS.json).  `req B/px`: the bytes the pass "
           "must move when staged (DESIGN.md section 7); `req frac` = those bytes over the pass time." % peak, "",
           "| dir | pass | us | DRAM MB | GB/s | frac | req B/px | req frac | warp instr | issue % |",
           "|---|---|---|---|---|---|---|---|---|---|"] + table
-    with open(os.path.join(ROOT, "profiles", "%s_passes_c5.md" % tag), "w") as f:
+    with open(os.path.join(ROOT, "profiles", "%s_passes_%s.md" % (tag, cfg.lower())), "w") as f:
         f.write("\n".join(md) + "\n")
     print("\n".join(md))
 
