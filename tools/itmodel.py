@@ -153,3 +153,70 @@ def run3():
             its.append(it)
         its = np.array(its)
         print("exact jumps shifted by <= %d: fine iters mean %.2f max %d" % (shift, its.mean(), its.max()))
+
+
+def pdas(y, lam, init_pos=None, init_neg=None, maxit=64):
+    """Primal-dual active set (semismooth Newton) on the same dual: the next bound set is
+    read off the partition candidate itself -- free edges with |uhat| > lam join with the
+    sign of uhat, bound edges stay iff the candidate jumps in their direction."""
+    n = len(y)
+    y = y - y.mean()
+    pin = np.zeros(n, bool)
+    pin[n - 1] = True
+    sp = np.zeros(n, bool) if init_pos is None else init_pos.copy()
+    sn = np.zeros(n, bool) if init_neg is None else init_neg.copy()
+    for it in range(maxit):
+        u = np.where(sp, lam, np.where(sn, -lam, 0.0))
+        bnd = pin | sp | sn
+        xh, uh = candidate(y, u, bnd)
+        dx = np.append(np.diff(xh), 0)
+        free = ~bnd
+        np_ = (free & (uh > lam * (1 + 1e-12) + 1e-12)) | (sp & (dx > 0))
+        nn_ = (free & (uh < -lam * (1 + 1e-12) - 1e-12)) | (sn & (dx < 0))
+        np_ &= ~pin
+        nn_ &= ~pin
+        if np.array_equal(np_, sp) and np.array_equal(nn_, sn):
+            return xh, it + 1
+        sp, sn = np_, nn_
+    return xh, maxit
+
+
+def run4():
+    w = workloads.c2(batch=256)
+    for name in ("cold", "coarse16"):
+        for solver in ("pn", "pdas"):
+            its, errs = [], []
+            for b in range(256):
+                y = w.y[b].astype(np.float64)
+                lam = float(w.lam[b])
+                p = q = None
+                if name != "cold":
+                    p, q, _ = coarse_pn_init(y, lam, 16)
+                xh, it = (pn if solver == "pn" else pdas)(y, lam, p, q)
+                ref = oracle.prox1d(y, lam)
+                errs.append(np.abs(xh + y.mean() - ref).max())
+                its.append(it)
+            its = np.array(its)
+            print("%-9s %-5s iters mean %.2f p99 %d max %d  maxerr %.1e" % (
+                name, solver, its.mean(), np.percentile(its, 99), its.max(), max(errs)))
+    # shifted exact jumps
+    w = workloads.c2(batch=128)
+    for shift in (1, 4):
+        for solver in ("pn", "pdas"):
+            its = []
+            for b in range(128):
+                y = w.y[b].astype(np.float64)
+                lam = float(w.lam[b])
+                x = oracle.prox1d(y, lam)
+                d = np.diff(x)
+                n = len(y)
+                pos = np.zeros(n, bool); neg = np.zeros(n, bool)
+                rng = np.random.default_rng(b)
+                for e in np.flatnonzero(np.abs(d) > 0):
+                    e2 = int(np.clip(e + rng.integers(-shift, shift + 1), 0, n - 2))
+                    if d[e] > 0: pos[e2] = True
+                    else: neg[e2] = True
+                _, it = (pn if solver == "pn" else pdas)(y, lam, pos, neg)
+                its.append(it)
+            its = np.array(its)
+            print("shift<=%d %-5s iters mean %.2f max %d" % (shift, solver, its.mean(), its.max()))
