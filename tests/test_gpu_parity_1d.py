@@ -260,6 +260,27 @@ def test_nonfinite_row_flagged(tp):
     check_forward(y[others], 0.5, x[others], mask[others], it[others], "f32")
 
 
+@pytest.mark.parametrize("n", [3000, 20000])
+def test_long_rows_edge_cases(tp, n):
+    """One-CTA and cluster long rows: lambda = 0 is a bitwise copy, a NaN row is flagged
+    without disturbing the others, huge lambda gives the row mean, a constant row is itself."""
+    y = workloads.random_rows(9980 + n, 4, n, "normal", np.float32)
+    x, mask, it = run_gpu(tp, y, 0.0, torch.float32)
+    assert np.array_equal(x, y) and np.all(it == 0)
+    y2 = y.copy()
+    y2[1, n // 3] = np.nan
+    x, mask, it = run_gpu(tp, y2, 0.5, torch.float32)
+    assert it[1] == -2 and np.all(np.isnan(x[1]))
+    check_forward(y2[[0, 2, 3]], 0.5, x[[0, 2, 3]], mask[[0, 2, 3]], it[[0, 2, 3]], "f32")
+    y64 = y.astype(np.float64)
+    lmax = np.abs(np.cumsum(y64 - y64.mean(1, keepdims=True), axis=1)[:, :-1]).max(1)
+    x, mask, it = run_gpu(tp, y64, lmax * 1.01, torch.float64)
+    np.testing.assert_allclose(x, np.repeat(y64.mean(1, keepdims=True), n, 1), atol=1e-9)
+    yc = np.repeat(y[:, :1], n, axis=1)
+    x, mask, it = run_gpu(tp, yc, 0.7, torch.float32)
+    assert np.abs(x - yc).max() <= 1e-6 * (np.abs(yc).max() + 1)
+
+
 def test_strided_rows(tp):
     base = workloads.random_rows(9600, 12, 333, "step", np.float32)
     yt = torch.as_tensor(base, device="cuda")[:, :300]      # stride 333 > n = 300

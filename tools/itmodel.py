@@ -220,3 +220,54 @@ def run4():
                 its.append(it)
             its = np.array(its)
             print("shift<=%d %-5s iters mean %.2f max %d" % (shift, solver, its.mean(), its.max()))
+
+
+def pn_eps(y, lam, init_pos=None, init_neg=None, maxit=64, eps=0.0):
+    """PN with Bertsekas' epsilon-active bound set: edges within eps*lam of the bound with an
+    outward gradient are bound (snapped to the bound)."""
+    n = len(y)
+    y = y - y.mean()
+    pin = np.zeros(n, bool)
+    pin[n - 1] = True
+    u = np.zeros(n)
+    bnd = pin.copy()
+    if init_pos is not None:
+        u[init_pos] = lam
+        u[init_neg] = -lam
+        bnd |= init_pos | init_neg
+    first = True
+    for it in range(maxit):
+        if not first:
+            x = y + u - np.concatenate([[0], u[:-1]])
+            g = np.append(np.diff(x), 0)
+            near = np.abs(u) >= lam * (1 - eps)
+            bnd = pin | (near & (u * g > 0))
+            u = np.where(bnd & ~pin, np.sign(u) * lam, u)
+        xh, uh = candidate(y, u, bnd)
+        free = ~bnd
+        feas = np.all(np.abs(uh[free]) <= lam * (1 + 1e-12) + 1e-12)
+        jb = bnd & ~pin
+        dx = np.append(np.diff(xh), 0)
+        sgn = np.all(u[jb] * dx[jb] >= -1e-12)
+        if feas and sgn:
+            return xh, it + 1
+        u = np.where(bnd, u, np.clip(uh, -lam, lam))
+        first = False
+    return xh, maxit
+
+
+def run5():
+    w = workloads.c2(batch=256)
+    for eps in (0.0, 0.01, 0.05, 0.1, 0.2, 0.4):
+        its, errs = [], []
+        for b in range(256):
+            y = w.y[b].astype(np.float64)
+            lam = float(w.lam[b])
+            p, q, _ = coarse_pn_init(y, lam, 16)
+            xh, it = pn_eps(y, lam, p, q, eps=eps)
+            ref = oracle.prox1d(y, lam)
+            errs.append(np.abs(xh + y.mean() - ref).max())
+            its.append(it)
+        its = np.array(its)
+        print("eps %.2f iters mean %.2f p99 %d max %d  maxerr %.1e" % (eps, its.mean(), np.percentile(its, 99),
+                                                                     its.max(), max(errs)))
