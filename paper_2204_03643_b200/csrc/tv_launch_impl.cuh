@@ -119,11 +119,15 @@ template <typename T, int E, int LPR> constexpr int col_wpb_fwd() {
 #ifndef TVP_COLB14_WPB
 #define TVP_COLB14_WPB 4
 #endif
+#ifndef TVP_COLB16_WPB
+#define TVP_COLB16_WPB 8
+#endif
 template <typename T, int E, int LPR> constexpr int col_wpb_bwd() {
 #ifdef TVP_COL_WPB
     return TVP_COL_WPB;
 #else
-    return (sizeof(T) == 4 && E == 14) ? TVP_COLB14_WPB : ((sizeof(T) == 8 && E == 32) ? 4 : 8);
+    return (sizeof(T) == 4 && E == 14) ? TVP_COLB14_WPB
+         : ((sizeof(T) == 4 && E == 16 && LPR == 32) ? TVP_COLB16_WPB : ((sizeof(T) == 8 && E == 32) ? 4 : 8));
 #endif
 }
 

@@ -162,7 +162,7 @@ def main():
                 agg[r[ki]].append(v)
         tot = sum(sum(v) for v in agg.values())
         out = ["# Launch list (%s): `ncu --metrics gpu__time_duration.sum --clock-control none` of "
-               "`python bench.py --steps 2 --warmup 3 --no-cpu-baseline`" % tag, "",
+               "`python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-configs --no-verify`" % tag, "",
                "Serialised, cold-cache per-launch times: compare SHARES, not absolutes.", "",
                "| kernel | launches | total ms | mean us | share |", "|---|---|---|---|---|"]
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
