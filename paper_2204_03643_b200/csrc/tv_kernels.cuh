@@ -1335,13 +1335,14 @@ k_col_bwd(ColBwdArgs<T> a) {
         const int64_t base = p * HW + c0;
         // the mask words of the warp's first column pair are loaded with the tile, so their
         // latency overlaps the tile's (the adjoint passes are latency-bound)
-        MaskWin<E> mpre;
-        {
-            const int cp = warp * G + grp;
-            if (cp < tcw && a.mw > 0) mask_words_ld<E>(a.mask + (p * W + c0 + cp) * a.mw, a.mw, l * E, mpre);
+        MaskWin<E> mpre[2];                 // the warp's (at most two) column groups of the tile
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int cp = (warp + rr * WPB) * G + grp;
+            if (cp < tcw && a.mw > 0) mask_words_ld<E>(a.mask + (p * W + c0 + cp) * a.mw, a.mw, l * E, mpre[rr]);
             else {
 #pragma unroll
-                for (int j = 0; j <= MaskWin<E>::NS; ++j) mpre.w[j] = 0u;
+                for (int j = 0; j <= MaskWin<E>::NS; ++j) mpre[rr].w[j] = 0u;
             }
         }
         if (tile_v4<T, TC>(W, tcw, reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.B ? a.B : a.A)) &&
@@ -1379,8 +1380,11 @@ k_col_bwd(ColBwdArgs<T> a) {
             T v[E];
             smem_to_regs<T, E>(bufV + c * LP, l, v);
             uint32_t bnd = 0, pos = 0, neg = 0;
-            if (cg == warp) {
-                if (a.mw > 0) mask_decode<E>(mpre, l * E, bnd, pos, neg);
+            if (cg < warp + 2 * WPB) {
+                MaskWin<E> m;
+#pragma unroll
+                for (int j = 0; j <= MaskWin<E>::NS; ++j) m.w[j] = cg == warp ? mpre[0].w[j] : mpre[1].w[j];
+                if (a.mw > 0) mask_decode<E>(m, l * E, bnd, pos, neg);
                 bnd |= pin_tail<E>(H - 1 - l * E);
             } else {
                 bwd_mask_bits<E>(a.mask + (valid ? (p * W + c0 + c) : 0) * a.mw, a.mw, H, l, bnd, pos, neg);
