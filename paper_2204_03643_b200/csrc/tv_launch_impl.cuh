@@ -109,11 +109,15 @@ static int row_fwd_split() {
 // TVP_COL_WPB forces one value for every column kernel (A/B builds).
 // fp64 lines of E = 32 (513..1024 samples) use 4 warps (8 columns): 8 would need
 // 2 x 16 x 1055 x 8 B = 270 KB of shared memory, above the 227 KB per-CTA limit.
+#ifndef TVP_COLF14_WPB
+#define TVP_COLF14_WPB 8
+#endif
 template <typename T, int E, int LPR> constexpr int col_wpb_fwd() {
 #ifdef TVP_COL_WPB
     return TVP_COL_WPB;
 #else
-    return ((sizeof(T) == 4 && E == 16 && LPR == 32) || (sizeof(T) == 8 && E == 32)) ? 4 : 8;
+    return (sizeof(T) == 4 && E == 14) ? TVP_COLF14_WPB
+         : (((sizeof(T) == 4 && E == 16 && LPR == 32) || (sizeof(T) == 8 && E == 32)) ? 4 : 8);
 #endif
 }
 #ifndef TVP_COLB14_WPB
