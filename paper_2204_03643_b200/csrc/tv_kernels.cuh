@@ -920,6 +920,19 @@ __device__ __forceinline__ void tile_st4(float* __restrict__ O0, float* __restri
 // ===========================================================================
 // Column forward: Dykstra column pass (tile of TC columns of one plane).
 // ===========================================================================
+// Column groups per warp in a forward column tile: 2 for the E = 14 (129..224-sample)
+// columns (C5 fwd 4.217 -> 4.154 ms), 1 elsewhere (C4 1.371 -> 1.456 ms with 2);
+// TVP_COLF_TM forces one value (A/B).
+template <typename T, int E> constexpr int colf_tm() {
+#ifdef TVP_COLF_TM
+    return TVP_COLF_TM;
+#else
+    return (sizeof(T) == 4 && E == 14) ? 2 : 1;
+#endif
+}
+#ifndef TVP_COLF_DYN
+#define TVP_COLF_DYN 0
+#endif
 template <typename T, int E, int LPR, int WPB, bool LSP>
 __global__ void __launch_bounds__(WPB * 32, (col_minb<T, E>()))
 k_col_fwd(ColFwdArgs<T> a) {
@@ -927,8 +940,9 @@ k_col_fwd(ColFwdArgs<T> a) {
     constexpr int LP = line_pitch<E, LPR>();
     extern __shared__ __align__(16) unsigned char smraw_[];
     T* bufA = reinterpret_cast<T*>(smraw_);
-    constexpr int TC = WPB * (32 / LPR) * (LPR == 32 ? 2 : 1);   // == col_tile<WPB, LPR>() of the launcher
+    constexpr int TC = WPB * (32 / LPR) * (LPR == 32 ? 2 : 1) * colf_tm<T, E>();   // == col_tile_fwd<...>()
     T* bufX = bufA + TC * LP;
+    __shared__ int s_cg;                      // dynamic column-group counter (TVP_COLF_DYN)
     uint32_t* mwb = reinterpret_cast<uint32_t*>(bufX + TC * LP) + (threadIdx.x >> 5) * 64;   // mask words
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
@@ -941,6 +955,7 @@ k_col_fwd(ColFwdArgs<T> a) {
         const int64_t p = tile / tpp;
         const int c0 = (int)(tile % tpp) * TC;
         const int tcw = min(TC, W - c0);
+        if (TVP_COLF_DYN && threadIdx.x == 0) s_cg = 0;     // read after the load barrier
         const int64_t base = p * HW + c0;
         // ---- coalesced load of the [H x TC] tile, transposed into line-major smem
         // (16-byte vectors of 4 columns when the tile is full and rows are aligned)
@@ -974,7 +989,17 @@ k_col_fwd(ColFwdArgs<T> a) {
         }
         __syncthreads();
         const T lamp = line_lambda(a.lam, a.lam_mode, a.lam_scalar, p, 1, a.C);
-        for (int cg = warp; cg < TC / G; cg += WPB) {
+        auto next_cg = [&](int cg) -> int {
+#if TVP_COLF_DYN
+            (void)cg;
+            int v = 0;
+            if (lane == 0) v = atomicAdd(&s_cg, 1);
+            return __shfl_sync(FULL, v, 0);
+#else
+            return cg + WPB;
+#endif
+        };
+        for (int cg = TVP_COLF_DYN ? next_cg(0) : warp; cg < TC / G; cg = next_cg(cg)) {
             const int c = cg * G + grp;
             const bool valid = c < tcw;
             T y[E], w[E];

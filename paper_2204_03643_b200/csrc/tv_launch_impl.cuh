@@ -288,12 +288,13 @@ cudaError_t launch_row_fwd_ls(RowFwdArgs<T> a, bool per_edge, bool dykstra, cuda
 }
 
 template <int WPB, int LPR> constexpr int col_tile() { return WPB * (32 / LPR) * (LPR == 32 ? 2 : 1); }
+template <typename T, int E, int WPB, int LPR> constexpr int col_tile_fwd() { return col_tile<WPB, LPR>() * colf_tm<T, E>(); }
 
 template <typename T, int E, int LPR, bool LSP>
 static cudaError_t col_fwd_t(ColFwdArgs<T> a, cudaStream_t s) {
     constexpr int WPB = col_wpb_fwd<T, E, LPR>();
     constexpr int LP = line_pitch<E, LPR>();
-    constexpr int TC = col_tile<WPB, LPR>();
+    constexpr int TC = col_tile_fwd<T, E, WPB, LPR>();
     a.TC = TC;
     if (LPR < 32 && !coarse16_knob()) a.coarse = 0;
     const size_t smem = (size_t)2 * TC * LP * sizeof(T) + (size_t)WPB * 64 * 4;
