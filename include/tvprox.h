@@ -216,7 +216,9 @@ size_t tv2d_workspace_bytes(tvp_dtype_t dt, int64_t N, int64_t C, int64_t H, int
  * saved nullable (inference).  workspace: tv2d_workspace_bytes(...) bytes.
  * line_iters nullable: int32 [K][2], max PN iterations over the lines of each
  * pass (row, column); a value >= 2^20 means some line of that pass did not
- * converge (diagnostics; written with integer atomics, deterministic).
+ * converge or was non-finite (diagnostics; written with integer atomics,
+ * deterministic).  A non-finite pixel makes its row NaN in row pass 1 and, from
+ * there, every line of its plane it reaches; other planes are unaffected.
  * Errors: TVP_EINVAL for NULL X/Y/workspace, N,C < 0, H,W < 1, iters < 1,
  * invalid lam; TVP_EUNSUPPORTED if H or W > tvp_max_line(dt).
  */

@@ -272,6 +272,26 @@ def test_in_place(tp, H, W):
     run_case(tp, X, [0.2, 0.5, 1.1], "channel", 4, in_place=True)
 
 
+@pytest.mark.parametrize("H,W,fused", [(56, 56, -1), (56, 56, 0), (224, 224, 0), (224, 224, 1), (40, 300, 0)])
+def test_nonfinite_pixel_isolated_to_its_plane(tp, H, W, fused):
+    """A NaN pixel poisons its own plane (its row, then the columns that row reaches) and
+    flags the passes as not converged; every other plane is exact (O21 per line)."""
+    rng = np.random.default_rng(H * 5 + W)
+    X = np.maximum(rng.standard_normal((2, 2, H, W)), 0).astype(np.float32)
+    X[1, 0, H // 3, W // 2] = np.nan
+    lam = np.array([0.3, 0.9], np.float32)
+    Y, saved, li = tp.tv2d_fwd(torch.as_tensor(X, device="cuda"), torch.as_tensor(lam, device="cuda"), 4,
+                               want_iters=True, opts=tp.make_options(fused2d=fused))
+    Y = Y.cpu().numpy().reshape(4, H, W)
+    assert np.isnan(Y[2]).any()
+    assert np.all(li.cpu().numpy()[0] >= (1 << 20))          # row pass 1 saw a non-finite line
+    good = [0, 1, 3]
+    Yr, _ = oracle.prox2d_batch(X.reshape(4, H, W)[good].astype(np.float64), np.tile(lam, 2)[good].astype(np.float64),
+                                4, nthreads=8)
+    assert np.all(np.isfinite(Y[good]))
+    assert np.abs(Y[good].astype(np.float64) - Yr).max() <= TOL["f32"] * rng_range(X.reshape(4, H, W)[good])
+
+
 @pytest.mark.parametrize("H,W", [(1024, 9), (9, 1024), (600, 20), (20, 600)])
 def test_fp64_long_lines(tp, H, W):
     """fp64 rows and columns of 513..1024 samples (E = 32 geometry; columns on 4-warp tiles
