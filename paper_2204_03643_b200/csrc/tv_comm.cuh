@@ -129,6 +129,8 @@ struct Comm {
         bool hx;        // a flagged lane strictly below this lane
         int rs;         // lowest flagged lane strictly above (absolute), valid if rf
         bool rf;
+        int Dr;         // reverse scans: adds allowed for levels d <= Dr (lowest flagged lane
+                        // >= this lane, else the group's last lane, minus this lane)
         uint32_t fm;    // ballot of the flags (whole warp)
     };
     __device__ __forceinline__ Seg seg_plan(bool f) const {
@@ -146,6 +148,8 @@ struct Comm {
         g.hx = (le & ~(1u << lane)) != 0u;
         g.rf = gt != 0u;
         g.rs = g.rf ? __ffs(gt) - 1 : (int)lane;
+        const uint32_t ge = fm & ghi & ~((1u << lane) - 1u);                          // flagged, >= lane
+        g.Dr = (ge ? __ffs(ge) - 1 : (int)(gb + LPR - 1)) - (int)lane;
         g.fm = fm;
         return g;
     }
@@ -200,18 +204,20 @@ struct Comm {
         a = ea;
         c = ecf & 0x3fffffff;
     }
-    // Segmented exclusive scan of two summed values (a, b).
+    // Reverse segmented exclusive scan of two summed values (a, b): each line lane gets the
+    // sums over the lanes strictly to its right up to and including the nearest flagged one
+    // (up to the line's end if none) -- the mirror image of a forward segmented scan.
     template <int S>
-    __device__ __forceinline__ void scan_fwd2(const Seg& g, T& a, T& b) const {
+    __device__ __forceinline__ void scan_rev2(const Seg& g, T& a, T& b) const {
 #pragma unroll
         for (int d = 1; d < LPR; d <<= 1) {
-            const T a2 = shup<LPR>(a, d), b2 = shup<LPR>(b, d);
-            if (d <= g.D) { a += a2; b += b2; }
+            const T a2 = shdn<LPR>(a, d), b2 = shdn<LPR>(b, d);
+            if (d <= g.Dr) { a += a2; b += b2; }
         }
-        T ea = shup<LPR>(a, 1), eb = shup<LPR>(b, 1);
-        if (l == 0) { ea = T(0); eb = T(0); }
+        T ea = shdn<LPR>(a, 1), eb = shdn<LPR>(b, 1);
+        if (l == LPR - 1) { ea = T(0); eb = T(0); }
         if (WPL > 1) {
-            if (l == LPR - 1) { V(S, 0, w) = a; V(S, 1, w) = b; I(S, w) = (int)g.hh; }
+            if (l == 0) { V(S, 0, w) = a; V(S, 1, w) = b; I(S, w) = (int)(g.fm != 0u); }
             __syncthreads();
             T ca = T(0), cb = T(0);
             if constexpr (WPL > 2) {
@@ -219,22 +225,22 @@ struct Comm {
                 int xf = (l < WPL) ? I(S, l) : 0;
 #pragma unroll
                 for (int d = 1; d < WPL; d <<= 1) {
-                    const T a2 = shup<32>(xa, d), b2 = shup<32>(xb, d);
-                    const int f2 = shup<32>(xf, d);
-                    if (l >= d && !xf) { xa += a2; xb += b2; xf = f2; }
+                    const T a2 = shdn<32>(xa, d), b2 = shdn<32>(xb, d);
+                    const int f2 = shdn<32>(xf, d);
+                    if (l + d < WPL && !xf) { xa += a2; xb += b2; xf = f2; }
                 }
-                ca = __shfl_sync(FULL, xa, w > 0 ? w - 1 : 0);
-                cb = __shfl_sync(FULL, xb, w > 0 ? w - 1 : 0);
-                if (w == 0) { ca = T(0); cb = T(0); }
+                ca = __shfl_sync(FULL, xa, w + 1 < WPL ? w + 1 : 0);
+                cb = __shfl_sync(FULL, xb, w + 1 < WPL ? w + 1 : 0);
+                if (w + 1 >= WPL) { ca = T(0); cb = T(0); }
             } else {
 #pragma unroll
-                for (int i = 0; i < WPL - 1; ++i) {
-                    if (i < w) {
+                for (int i = WPL - 1; i >= 1; --i) {
+                    if (i > w) {
                         if (I(S, i)) { ca = V(S, 0, i); cb = V(S, 1, i); } else { ca += V(S, 0, i); cb += V(S, 1, i); }
                     }
                 }
             }
-            if (!g.hx) { ea += ca; eb += cb; }
+            if (!g.rf) { ea += ca; eb += cb; }
         }
         a = ea;
         b = eb;

@@ -1467,6 +1467,7 @@ struct PlaneFwdArgs {
     int32_t* diag;            // nullable: accumulated line counters (line_diag)
     int32_t* hist;            // nullable: [2K][kHistBins] (pass 2(k-1) rows, 2(k-1)+1 columns)
     int coarse;               // cold passes (k = 1) start from the coarse bound set (cluster kernels)
+    int pw;                   // shared-memory row pitch of the plane state (plane_pitch, host side)
 };
 
 #ifndef TVP_PLANE_DYN
@@ -1482,7 +1483,7 @@ k_plane_fwd(PlaneFwdArgs<T> a) {
     constexpr int LPR = 8, G = 4;                     // 8 lanes per line, 4 lines per warp
     extern __shared__ __align__(16) unsigned char smraw_[];
     const int H = a.H, W = a.W, K = a.K;
-    const int PW = W | 1;                             // odd pitch: conflict-free column reads
+    const int PW = a.pw;                              // bank-conflict-minimising pitch (plane_pitch)
     T* ys = reinterpret_cast<T*>(smraw_);
     T* ps = ys + H * PW;
     T* qs = ps + H * PW;
@@ -1654,6 +1655,7 @@ struct PlaneBwdArgs {
     int H, W, K;
     int mwr, mwc;
     T* lampart;               // nullable: [plane][k][H + W] partials
+    int pw;                   // shared-memory row pitch of the adjoint planes (plane_pitch)
 };
 
 template <typename T, int ER, int EC, int WPB>
@@ -1661,7 +1663,7 @@ __global__ void __launch_bounds__(WPB * 32) k_plane_bwd(PlaneBwdArgs<T> a) {
     constexpr int LPR = 8, G = 4;
     extern __shared__ __align__(16) unsigned char smraw_[];
     const int H = a.H, W = a.W, K = a.K;
-    const int PW = W | 1;
+    const int PW = a.pw;
     T* As = reinterpret_cast<T*>(smraw_);
     T* Bs = As + H * PW;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -1,5 +1,6 @@
 // tv_launch_impl.cuh -- launcher templates (included once per dtype unit).
 #pragma once
+#include <atomic>
 #include <algorithm>
 #include <mutex>
 #include <unordered_map>
@@ -440,14 +441,64 @@ cudaError_t launch_axpby(const T* x, T* y, T a, T b, int64_t n, cudaStream_t s) 
     return cudaGetLastError();
 }
 
+// Shared-memory row pitch of the fused plane kernels' [H][pitch] planes.  A warp reads 4 lines
+// x 8 lanes: row pass lanes (g, l) at (4t + g, ER l + q), column pass at (EC l + q, 4t + g).
+// For fp32 the pitch in [W, W + 32) with the fewest bank conflicts over both patterns (max
+// ways, then total) is chosen once per (H, W); e.g. C3's 56 x 56 planes get pitch 56 (row
+// reads 2-way, column reads conflict-free) instead of the odd pitch 57 (4-way / 2-way).
+// fp64 keeps the odd pitch.
+inline int plane_conflicts(int P, int ER, int EC, int H, int W, int& sum) {
+    int worst = 0;
+    sum = 0;
+    for (int o = 0; o < 2; ++o) {
+        const int E = o ? EC : ER, nl = o ? W : H, ne = o ? H : W;
+        int wo = 0;
+        for (int t = 0; t < (nl + 3) / 4 && t < 8; ++t)        // the bank pattern repeats in t with period 8
+            for (int q = 0; q < E; ++q) {
+                int cnt[32] = {0};
+                for (int g = 0; g < 4; ++g)
+                    for (int l = 0; l < 8; ++l) {
+                        const int line = 4 * t + g, e = E * l + q;
+                        if (line >= nl || e >= ne) continue;
+                        const int h = o ? e : line, c = o ? line : e;
+                        const int b = (h * P + c) & 31;
+                        if (++cnt[b] > wo) wo = cnt[b];
+                    }
+            }
+        worst = wo > worst ? wo : worst;
+        sum += wo;
+    }
+    return worst;
+}
+template <typename T>
+inline int plane_pitch(int H, int W, int ER, int EC) {
+    if (sizeof(T) != 4 || H < 1 || H > 64 || W < 1 || W > 64) return W | 1;
+    static std::atomic<int> cache[2][2][65][65];       // [ER==8][EC==8][H][W], 0 = not computed
+    std::atomic<int>& c = cache[ER == 8][EC == 8][H][W];
+    int v = c.load(std::memory_order_relaxed);
+    if (v == 0) {
+        int bw = 1 << 30, bs = 1 << 30;
+        v = W | 1;
+        for (int P = W; P < W + 32; ++P) {
+            int sum;
+            const int wv = plane_conflicts(P, ER, EC, H, W, sum);
+            if (wv < bw || (wv == bw && sum < bs)) { v = P; bw = wv; bs = sum; }
+        }
+        c.store(v, std::memory_order_relaxed);         // idempotent: racing callers store the same value
+    }
+    return v;
+}
+
 // f2 fused plane forward (32 < H, W <= 64); E per orientation as in the staged passes
 #ifndef TVP_PLANE_WPB
 #define TVP_PLANE_WPB 8
 #endif
 template <typename T, int ER, int EC, bool LSP>
-static cudaError_t plane_fwd_t(const PlaneFwdArgs<T>& a, cudaStream_t s) {
+static cudaError_t plane_fwd_t(const PlaneFwdArgs<T>& a0, cudaStream_t s) {
     constexpr int WPB = TVP_PLANE_WPB;
-    const int PW = a.W | 1;
+    PlaneFwdArgs<T> a = a0;
+    a.pw = plane_pitch<T>(a.H, a.W, ER, EC);
+    const int PW = a.pw;
     const size_t smem = (size_t)3 * a.H * PW * sizeof(T) + (size_t)WPB * 32 * 4 + (size_t)4 * 16 * 32 * 4;
     auto kern = k_plane_fwd<T, ER, EC, WPB, LSP>;
     int grid = 0;
@@ -468,9 +519,11 @@ cudaError_t launch_plane_fwd_ls(const PlaneFwdArgs<T>& a, cudaStream_t s) {
 }
 
 template <typename T, int ER, int EC>
-static cudaError_t plane_bwd_t(const PlaneBwdArgs<T>& a, cudaStream_t s) {
+static cudaError_t plane_bwd_t(const PlaneBwdArgs<T>& a0, cudaStream_t s) {
     constexpr int WPB = TVP_PLANE_WPB;
-    const int PW = a.W | 1;
+    PlaneBwdArgs<T> a = a0;
+    a.pw = plane_pitch<T>(a.H, a.W, ER, EC);
+    const int PW = a.pw;
     const size_t smem = (size_t)2 * a.H * PW * sizeof(T);
     auto kern = k_plane_bwd<T, ER, EC, WPB>;
     int grid = 0;

@@ -93,30 +93,28 @@ template <int E, int WPL> constexpr bool seg_ptx() {
 // edge (bit b of nb) the segment value num / cnt (num itself on the lane's first bound,
 // which still lacks its carry) is stored and the running sums restart.
 __device__ __forceinline__ void seg_step(uint32_t nb, uint32_t fbm, uint32_t b, float num, float cnt, float uk,
-                                         float& w, float& numf, float& ub, float& s, float& c) {
+                                         float& w, float& numf, float& s, float& c) {
     asm("{\n\t.reg .pred pb, pf;\n\t.reg .b32 t1, t2;\n\t.reg .f32 r, v;\n\t"
-        "and.b32 t1, %5, %7;\n\t"
+        "and.b32 t1, %4, %6;\n\t"
         "setp.ne.u32 pb, t1, 0;\n\t"
-        "and.b32 t2, %6, %7;\n\t"
+        "and.b32 t2, %5, %6;\n\t"
         "setp.ne.u32 pf, t2, 0;\n\t"
-        "rcp.approx.ftz.f32 r, %9;\n\t"
-        "mul.f32 v, %8, r;\n\t"
-        "@pf mov.f32 v, %8;\n\t"
-        "@pf mov.f32 %1, %8;\n\t"
+        "rcp.approx.ftz.f32 r, %8;\n\t"
+        "mul.f32 v, %7, r;\n\t"
+        "@pf mov.f32 v, %7;\n\t"
+        "@pf mov.f32 %1, %7;\n\t"
         "@pb mov.f32 %0, v;\n\t"
-        "@pb mov.f32 %2, %10;\n\t"
-        "@pb neg.f32 %3, %10;\n\t"
-        "@pb mov.f32 %4, 0f00000000;\n\t}"
-        : "+f"(w), "+f"(numf), "+f"(ub), "+f"(s), "+f"(c)
+        "@pb neg.f32 %2, %9;\n\t"
+        "@pb mov.f32 %3, 0f00000000;\n\t}"
+        : "+f"(w), "+f"(numf), "+f"(s), "+f"(c)
         : "r"(nb), "r"(fbm), "r"(b), "f"(num), "f"(cnt), "f"(uk));
 }
 __device__ __forceinline__ void seg_step(uint32_t nb, uint32_t fbm, uint32_t b, double num, double cnt, double uk,
-                                         double& w, double& numf, double& ub, double& s, double& c) {
+                                         double& w, double& numf, double& s, double& c) {
     const bool bk = (nb & b) != 0u, fk = (fbm & b) != 0u;
     const double val = fk ? num : num * rcp_(cnt);
     numf = fk ? num : numf;
     w = bk ? val : w;
-    ub = bk ? uk : ub;
     s = bk ? -uk : s;
     c = bk ? 0.0 : c;
 }
@@ -218,6 +216,38 @@ __device__ __forceinline__ void p4_restart(uint32_t bnd, uint32_t b, double uk, 
     A = bk ? fabs(uk) : A + fabs(t);
 }
 
+// Selects of the reverse P3/P4 pass: xhat_k = fv on the lane's first segment (bits 0..fb),
+// else the segment value w_k on a bound edge, else xhat_{k+1}; uhat_k = u_k and its slack
+// scale |u_k| restart on a bound edge, else the values carried from edge k + 1.
+__device__ __forceinline__ void p34_sel(uint32_t bnd, uint32_t firstm, uint32_t b, float fv, float wk, float xr,
+                                        float uk, float rr, float aa, float& xh, float& r, float& A) {
+    // (results built in asm-local registers: "=f" outputs may share a register with an input)
+    asm("{\n\t.reg .pred pb, pf;\n\t.reg .b32 t1, t2;\n\t.reg .f32 x, rv, av;\n\t"
+        "and.b32 t1, %3, %5;\n\t"
+        "setp.ne.u32 pb, t1, 0;\n\t"
+        "and.b32 t2, %4, %5;\n\t"
+        "setp.ne.u32 pf, t2, 0;\n\t"
+        "mov.f32 x, %8;\n\t"
+        "@pb mov.f32 x, %7;\n\t"
+        "@pf mov.f32 x, %6;\n\t"
+        "mov.f32 rv, %10;\n\t"
+        "@pb mov.f32 rv, %9;\n\t"
+        "mov.f32 av, %11;\n\t"
+        "@pb abs.f32 av, %9;\n\t"
+        "mov.f32 %0, x;\n\t"
+        "mov.f32 %1, rv;\n\t"
+        "mov.f32 %2, av;\n\t}"
+        : "=f"(xh), "=f"(r), "=f"(A)
+        : "r"(bnd), "r"(firstm), "r"(b), "f"(fv), "f"(wk), "f"(xr), "f"(uk), "f"(rr), "f"(aa));
+}
+__device__ __forceinline__ void p34_sel(uint32_t bnd, uint32_t firstm, uint32_t b, double fv, double wk, double xr,
+                                        double uk, double rr, double aa, double& xh, double& r, double& A) {
+    const bool bk = (bnd & b) != 0u;
+    xh = (firstm & b) ? fv : (bk ? wk : xr);
+    r = bk ? uk : rr;
+    A = bk ? fabs(uk) : aa;
+}
+
 // m |= b  iff  ug > 0 and au >= thr, as two compares (the second predicated on the
 // first) and one predicated OR -- the ALU pipe is the forward's binding pipe.
 __device__ __forceinline__ void or_if_outward(uint32_t& m, float ug, float au, float thr, uint32_t b) {
@@ -279,6 +309,14 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
     uint32_t bnd2 = 0xffffffffu;       // bound set two iterations ago (cycle detection)
     uint32_t bnd3 = 0xffffffffu, bnd4 = 0xffffffffu;   // three / four ago (cluster lines only)
     const T ynext = C.template next<1>(y[0]);
+    // lane constants of the reverse uhat carry (P3/P4): sum of |y| over the lane's samples
+    // and the largest lambda of the lane
+    T yabs = T(0), lmaxl = lam.at(0);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        yabs += fabs(y[k]);
+        if (PE) lmaxl = fmax(lmaxl, lam.at(k));
+    }
     const T eps = Num<T>::eps;
     const T slackA = eps * T(8);     // summation-error slack of the KKT test (x sum |terms|)
     const T slack1 = T(1) + T(2) * eps;
@@ -316,21 +354,20 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         const uint32_t nb = keep | outb;
         const uint32_t firstb = nb & (0u - nb);         // lowest bound edge of the lane
         // (b) lane-local segment numerators / values with the final bits
-        T s = T(0), cnt = T(0), numf = T(0), ub = T(0);
+        T s = T(0), cnt = T(0), numf = T(0);
 #pragma unroll
         for (int k = 0; k < E; ++k) {
             s += y[k];
             cnt += T(1);
             const T num = s + u[k];
             if constexpr (seg_ptx<E, WPL>()) {
-                seg_step(nb, firstb, 1u << k, num, cnt, u[k], w[k], numf, ub, s, cnt);
+                seg_step(nb, firstb, 1u << k, num, cnt, u[k], w[k], numf, s, cnt);
             } else {
                 const bool bk = bit<E>(nb, k);
                 const bool fk = bit<E>(firstb, k);
                 const T val = fk ? num : num * rcp_(cnt);
                 numf = fk ? num : numf;
                 w[k] = bk ? val : w[k];
-                ub = bk ? u[k] : ub;
                 s = bk ? -u[k] : s;
                 cnt = bk ? T(0) : cnt;
             }
@@ -366,105 +403,181 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         const auto sg = C.seg_plan(fl);               // segment geometry of this step's scans
         C.template scan_fwd<2, E>(sg, cs, cc);
 
-        // ---------------- P2/P3: the lane's first segment gets the carry; reverse
-        // broadcast of each segment's value to its samples.
+        // ---------------- P2: the lane's first segment gets the carry.
         const int fb = __ffs(bnd) - 1;                // -1 if none
         const uint32_t firstm = bnd ? ((bnd & (0u - bnd)) * 2u - 1u) : 0u;   // bits 0..fb
         const T fv = (numf + cs) * rcp_(T(fb + 1 + cc));
+        // lane aggregates of the reverse uhat carry (P3/P4 below); the flagless lanes' parts
+        // that need the value from the right are added after it arrives
+        T rr = fl ? (numf - T(fb + 1) * fv) : s;
+        T AA = fl ? (lmaxl + T(fb + 1) * fabs(fv)) + yabs : yabs;
+        // value of the segment that runs into this lane from the right: the first-segment
+        // value fv of the nearest flagged line lane to the right.  It is also xhat of the
+        // next line lane's first sample (that lane's fv if it is flagged, else the value it
+        // receives from the same source), so no neighbour exchange is needed for it.
         T cur = C.template scan_rev<3>(sg, fv);
-        // (the same reverse pass sums xhat - y over the lane's open tail: the lane
-        // aggregate of the uhat scan below, accumulated term by term)
-        const uint32_t tailm = fl ? ~((2u << hb) - 1u) : 0xffffffffu;
-        T rt = T(0), at = T(0);
+        bool ok = true, clip = false, chg = false;
+        bool lsmode;
+        if constexpr (CM::kCluster) {
+            // Lines held by a thread-block cluster (f4) keep the forward form of P3/P4: a
+            // reverse broadcast pass that also sums xhat - y over the lane's open tail, a
+            // forward segmented scan of (uhat, slack scale) from each segment's left end, and
+            // a forward KKT / step pass -- with explicit change detection for the stall rule
+            // (their cycle handling switches lines to the Armijo step, see above).
+            const uint32_t tailm = fl ? ~((2u << hb) - 1u) : 0xffffffffu;
+            T rt = T(0), at = T(0), ub = T(0);
 #pragma unroll
-        for (int k = E - 1; k >= 0; --k) {
-            T v;
-            if constexpr (p3_ptx<E, LPR, WPL>()) {
-                p3_step(bnd, firstm, 1u << k, fv, w[k], cur);
-                v = w[k];
-            } else {
-                v = bit<E>(bnd, k) ? w[k] : cur;
+            for (int k = 0; k < E; ++k) ub = bit<E>(bnd, k) ? u[k] : ub;     // u at the lane's last bound edge
+            const T xnext = cur;
+#pragma unroll
+            for (int k = E - 1; k >= 0; --k) {
+                T v = bit<E>(bnd, k) ? w[k] : cur;
                 v = bit<E>(firstm, k) ? fv : v;
                 w[k] = v;
+                cur = v;
+                const T t = v - y[k];
+                padd2(tailm, 1u << k, rt, t, at, fabs(t));
             }
-            cur = v;
-            const T t = v - y[k];
-            padd2(tailm, 1u << k, rt, t, at, fabs(t));
-        }
-        if (fin) break;
-
-        // ---------------- P4: KKT / zero-duality-gap test of the candidate and uhat.
-        // uhat_i = u_{a-1} + sum_{j=a..i} (xhat_j - y_j); free edges must satisfy
-        // |uhat_i| <= lam_i (up to a summation-error slack), bound edges must jump
-        // in the direction of u_i.  Fast mode (no line search possible this
-        // iteration) applies the projected full Newton step u <- clip(uhat) in the
-        // same pass and keeps xhat in w; LS mode writes uhat to w for the search.
-        T r = ub + rt;
-        T A = fabs(ub) + at;
-        C.template scan_fwd2<4>(sg, r, A);
-        const T xnext = C.template next<5>(w[0]);
-        const bool lsmode = C.uany(run && !first && (it + 1 >= ls_after));
-        bool ok = true, clip = false, chg = false;
-        if (!lsmode) {
-            // The tests accumulate non-negative violations on the FMA pipe instead of
-            // predicate logic (the ALU pipe binds this loop):
-            //  * r, A restart at bound edges (r = u_i there, so |r| <= lam_i never
-            //    reads as infeasible and clamp(r) = u_i keeps the bound value);
-            //  * sign test u_i (xhat_{i+1} - xhat_i) >= 0 needs no bound mask: across a
-            //    free edge both samples carry the same segment value bitwise (product 0),
-            //    and pinned edges have u = 0;
-            //  * |q| - q > 0 iff q < 0 and e + |e| > 0 iff e > 0, exactly (no FTZ), and
-            //    a sum of non-negative terms is 0 iff every term is.
-            T vio = T(0), dch = T(0);
+            if (fin) break;
+            T r = ub + rt;
+            T A = fabs(ub) + at;
+            C.template scan_fwd2<4>(sg, r, A);
+            lsmode = C.uany(run && !first && (it + 1 >= ls_after));
+            if (!lsmode) {
+                T vio = T(0), dch = T(0);
 #pragma unroll
-            for (int k = 0; k < E; ++k) {
-                const T xh = w[k];
-                const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
-                const T t = xh - y[k];
-                const T lk = lam.at(k);
-                if constexpr (p4_ptx<E, LPR, WPL>()) {
+                for (int k = 0; k < E; ++k) {
+                    const T xh = w[k];
+                    const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
+                    const T t = xh - y[k];
+                    const T lk = lam.at(k);
                     p4_restart(bnd, 1u << k, u[k], t, r, A);
-                } else {
-                    const bool bk = bit<E>(bnd, k);
-                    r = bk ? u[k] : r + t;
-                    A = bk ? fabs(u[k]) : A + fabs(t);
+                    const T q = u[k] * (xh1 - xh);
+                    const T e = fabs(r) - fma(slackA, A, lk * slack1);
+                    vio += (fabs(q) - q) + (e + fabs(e));
+                    dch += fabs(r - u[k]);
+                    u[k] = clampv(r, -lk, lk);
                 }
-                const T q = u[k] * (xh1 - xh);
-                const T e = fabs(r) - fma(slackA, A, lk * slack1);
-                vio += (fabs(q) - q) + (e + fabs(e));
-                dch += fabs(r - u[k]);
-                u[k] = clampv(r, -lk, lk);
-            }
-            ok = vio == T(0);
-            chg = dch != T(0);
-        } else {
+                ok = vio == T(0);
+                chg = dch != T(0);
+            } else {
 #pragma unroll
-            for (int k = 0; k < E; ++k) {
-                const T xh = w[k];
-                const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
-                const T t = xh - y[k];
-                r += t;
-                A += fabs(t);
-                const T lk = lam.at(k);
-                const bool bk = bit<E>(bnd, k);
-                const bool sgn_bad = (u[k] * (xh1 - xh) < T(0)) & !bit<E>(pin, k);
-                const T ar = fabs(r);
-                const bool infeas = ar > fma(slackA, A, lk * slack1);
-                ok = ok & !(bk ? sgn_bad : infeas);
-                clip = clip | (!bk & (ar > lk));
-                chg = chg | (!bk & (r != u[k]));
-                w[k] = bk ? u[k] : r;
-                A = bk ? fabs(u[k]) : A;
-                r = bk ? u[k] : r;
+                for (int k = 0; k < E; ++k) {
+                    const T xh = w[k];
+                    const T xh1 = (k + 1 < E) ? w[(k + 1 < E) ? k + 1 : k] : xnext;
+                    const T t = xh - y[k];
+                    r += t;
+                    A += fabs(t);
+                    const T lk = lam.at(k);
+                    const bool bk = bit<E>(bnd, k);
+                    const bool sgn_bad = u[k] * (xh1 - xh) < T(0);      // pinned edges: u = 0
+                    const T ar = fabs(r);
+                    const bool infeas = ar > fma(slackA, A, lk * slack1);
+                    ok = ok & !(bk ? sgn_bad : infeas);
+                    clip = clip | (!bk & (ar > lk));
+                    chg = chg | (!bk & (r != u[k]));
+                    w[k] = bk ? u[k] : r;
+                    A = bk ? fabs(u[k]) : A;
+                    r = bk ? u[k] : r;
+                }
+                clip = C.any(clip);
             }
-            clip = C.any(clip);
+            chg = C.any(chg);
+        } else {
+            if (fin) {
+                // final candidate pass: reverse broadcast of each segment's value to its samples
+#pragma unroll
+                for (int k = E - 1; k >= 0; --k) {
+                    T v;
+                    if constexpr (p3_ptx<E, LPR, WPL>()) {
+                        p3_step(bnd, firstm, 1u << k, fv, w[k], cur);
+                        v = w[k];
+                    } else {
+                        v = bit<E>(bnd, k) ? w[k] : cur;
+                        v = bit<E>(firstm, k) ? fv : v;
+                        w[k] = v;
+                    }
+                    cur = v;
+                }
+                break;
+            }
+
+            // ---------------- P3/P4 (one reverse pass): broadcast of the segment values, KKT /
+            // zero-duality-gap test of the candidate, and the dual uhat computed from each
+            // segment's right end:  uhat_{b-1} = u_{b-1} on a bound edge b-1 and, on a free edge,
+            //     uhat_i = uhat_{i+1} - (xhat_{i+1} - y_{i+1})
+            // (the same uhat as the running sum from the left end, since the partition value
+            // makes each segment's sum of xhat - y equal u_{b-1} - u_{a-1}).  Free edges must
+            // satisfy |uhat_i| <= lam_i (up to a summation-error slack), bound edges must jump in
+            // the direction of u_i.  Fast mode (no line search possible this iteration) applies
+            // the projected full Newton step u <- clip(uhat) in the same pass and keeps xhat in w;
+            // LS mode writes uhat to w for the search.
+            // The carry into the lane's last edge is a reverse segmented scan of the lanes' sums
+            // of -(xhat - y), O(1) per lane: a flagged lane's head [0, fb] sums to
+            // -((fb+1) fv - (numf - u_fb)) = numf - (fb+1) fv - u_fb, so it hands u_fb - that =
+            // numf - (fb+1) fv to its left; a flagless lane sums to E cur - s (s = its sample sum
+            // from P1b).  The slack scale carried with it is an upper bound of the matching
+            // |u| + sum |xhat - y| (|xhat - y_j| <= |xhat| + |y_j|).
+            if (!fl) {
+                rr -= T(E) * cur;
+                AA += T(E) * fabs(cur);
+            }
+            C.template scan_rev2<4>(sg, rr, AA);
+            lsmode = C.uany(run && !first && (it + 1 >= ls_after));
+            T xr = cur;                                   // xhat_{k+1}
+            if (!lsmode) {
+                // The tests accumulate non-negative violations on the FMA pipe instead of
+                // predicate logic (the ALU pipe binds this loop):
+                //  * r, A restart at bound edges (r = u_i there, so |r| <= lam_i never
+                //    reads as infeasible and clamp(r) = u_i keeps the bound value);
+                //  * sign test u_i (xhat_{i+1} - xhat_i) >= 0 needs no bound mask: across a
+                //    free edge both samples carry the same segment value bitwise (product 0),
+                //    and pinned edges have u = 0;
+                //  * |q| - q > 0 iff q < 0 and e + |e| > 0 iff e > 0, exactly (no FTZ), and
+                //    a sum of non-negative terms is 0 iff every term is.
+                T vio = T(0);
+#pragma unroll
+                for (int k = E - 1; k >= 0; --k) {
+                    T xh, r, A;
+                    p34_sel(bnd, firstm, 1u << k, fv, w[k], xr, u[k], rr, AA, xh, r, A);
+                    const T lk = lam.at(k);
+                    const T q = u[k] * (xr - xh);
+                    const T e = fabs(r) - fma(slackA, A, lk * slack1);
+                    vio += (fabs(q) - q) + (e + fabs(e));
+                    const T t = xh - y[k];
+                    rr = r - t;
+                    AA = A + fabs(t);
+                    u[k] = clampv(r, -lk, lk);
+                    w[k] = xh;
+                    xr = xh;
+                }
+                ok = vio == T(0);
+            } else {
+#pragma unroll
+                for (int k = E - 1; k >= 0; --k) {
+                    T xh, r, A;
+                    p34_sel(bnd, firstm, 1u << k, fv, w[k], xr, u[k], rr, AA, xh, r, A);
+                    const T lk = lam.at(k);
+                    const bool bk = bit<E>(bnd, k);
+                    const bool sgn_bad = u[k] * (xr - xh) < T(0);      // pinned edges: u = 0
+                    const T ar = fabs(r);
+                    const bool infeas = ar > fma(slackA, A, lk * slack1);
+                    ok = ok & !(bk ? sgn_bad : infeas);
+                    clip = clip | (!bk & (ar > lk));
+                    const T t = xh - y[k];
+                    rr = r - t;
+                    AA = A + fabs(t);
+                    w[k] = r;                             // uhat (u_k on bound edges)
+                    xr = xh;
+                }
+                clip = C.any(clip);
+            }
         }
         ok = C.all(ok);
-        chg = C.any(chg);
 #ifdef TVP_DEBUG
         if (active && C.first_lane())
-            printf("[tvp] itw %d it %d run %d first %d ok %d clip %d chg %d bchg %d uchg %d nbound %d ls %d\n", itw, it,
-                   (int)run, (int)first, (int)ok, (int)clip, (int)chg, (int)bchg, (int)uchg, __popc(bnd), (int)lsmode);
+            printf("[tvp] itw %d it %d run %d first %d ok %d clip %d bchg %d uchg %d nbound %d ls %d\n", itw, it,
+                   (int)run, (int)first, (int)ok, (int)clip, (int)bchg, (int)uchg, __popc(bnd), (int)lsmode);
 #endif
         if (run) ++it;
         if (run && ok) { conv = true; run = false; }
@@ -480,16 +593,21 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         // ---------------- step (LS mode): full Newton step when it stays in the box,
         // else the projected Armijo line search with quadratic-interpolation
         // backtracking of P:188 -- the globalisation safeguard from iteration ls_after on.
+        // After a full (projected) Newton step the next candidate depends only on the next
+        // bound set (xhat reads u on bound edges, which keep their values), so a bound set
+        // equal to this one reproduces this failed candidate bitwise: the step is a
+        // rounding-level fixed point, detected by bchg alone (uchg = false).  Only an
+        // Armijo step (below) changes u without changing the candidate.
         const bool fast = lsmode && run && (first || !clip);
         if (!lsmode) {
-            uchg = chg || first;
+            uchg = (CM::kCluster && chg) || first;
         } else if (fast) {
 #pragma unroll
             for (int k = 0; k < E; ++k) {
                 const T lk = lam.at(k);
                 u[k] = bit<E>(bnd, k) ? u[k] : clampv(w[k], -lk, lk);
             }
-            uchg = chg || first;
+            uchg = (CM::kCluster && chg) || first;
         }
         bool pending = lsmode && run && !fast;
         if (LSP && C.uany(pending)) {

@@ -271,3 +271,71 @@ def run5():
         its = np.array(its)
         print("eps %.2f iters mean %.2f p99 %d max %d  maxerr %.1e" % (eps, its.mean(), np.percentile(its, 99),
                                                                      its.max(), max(errs)))
+
+
+def dykstra_model(X, lam, K=4, prune=False):
+    """fp64 model of the staged 2D Dykstra passes with warm starts from the previous
+    same-orientation jump set; prune=True drops warm edges whose jump sign disagrees with
+    the primal at the previous pass's dual (x(u_{k-1}) = the pass input minus P / Q, i.e.
+    the current Y for rows and Z for columns).  Returns per-pass mean PN iterations."""
+    H, W = X.shape
+    Y = X.copy()
+    P = np.zeros_like(X)
+    Q = np.zeros_like(X)
+    mr = mc = None
+    its = []
+    for k in range(K):
+        A = Y + P
+        Z = np.empty_like(X)
+        nm = (np.zeros((H, W), bool), np.zeros((H, W), bool))
+        itr = []
+        for i in range(H):
+            p = q = None
+            if mr is not None:
+                p, q = mr[0][i].copy(), mr[1][i].copy()
+                if prune:
+                    d = np.append(np.diff(Y[i]), 0)
+                    p &= d > 0
+                    q &= d < 0
+            xh, it = pn(A[i], lam, p, q)
+            Z[i] = xh + A[i].mean()
+            d = np.append(np.diff(Z[i]), 0)
+            nm[0][i] = d > 0
+            nm[1][i] = d < 0
+            itr.append(it)
+        mr = nm
+        P = A - Z
+        B = Z + Q
+        Yn = np.empty_like(X)
+        nm = (np.zeros((W, H), bool), np.zeros((W, H), bool))
+        itc = []
+        for j in range(W):
+            p = q = None
+            if mc is not None:
+                p, q = mc[0][j].copy(), mc[1][j].copy()
+                if prune:
+                    d = np.append(np.diff(Z[:, j]), 0)
+                    p &= d > 0
+                    q &= d < 0
+            xh, it = pn(B[:, j], lam, p, q)
+            Yn[:, j] = xh + B[:, j].mean()
+            d = np.append(np.diff(Yn[:, j]), 0)
+            nm[0][j] = d > 0
+            nm[1][j] = d < 0
+            itc.append(it)
+        mc = nm
+        Q = B - Yn
+        Y = Yn
+        its += [np.mean(itr), np.mean(itc)]
+    return Y, its
+
+
+def run6(planes=3, H=224):
+    w = workloads.c5(N=1, C=3, H=H, W=H, with_grad=False)
+    for c in range(min(planes, 3)):
+        X = w.X[0, c].astype(np.float64)
+        lam = float(w.lam[c])
+        Ya, ia = dykstra_model(X, lam)
+        Yb, ib = dykstra_model(X, lam, prune=True)
+        print("plane %d lam %.3f  warm: %s" % (c, lam, " ".join("%.2f" % v for v in ia)))
+        print("             pruned: %s   |dY| %.1e" % (" ".join("%.2f" % v for v in ib), np.abs(Ya - Yb).max()))
