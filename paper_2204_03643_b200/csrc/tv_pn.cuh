@@ -322,11 +322,17 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
     const T slack1 = T(1) + T(2) * eps;
     const int maxit = max_iters > 0 ? max_iters : Num<T>::max_iters;
 
-    bool run = active, first = true, fin = false, uchg = true, fin_direct = false;
-    bool conv = false, stall = false;
+    // Line state.  Only run / fin / uchg are bools across the loop, the exit kind is an int
+    // and `first` is itw == 0: the per-sample loops need the predicate registers (with more
+    // long-lived bools the compiler packs predicates into a register, two LOP3 per save /
+    // restore, inside those loops).  Same-box A/B: C2 fwd 1.207 -> 1.133 ms, C5 4.08 -> 3.94;
+    // turning fin / uchg (and solve_line's active / bad) into ints as well measured slower.
+    bool run = active, fin = false, uchg = true;
+    int how = 0;                       // 1: converged, 2: accepted at a stall
     int it = 0;
     ls_passes = 0;
     for (int itw = 0;; ++itw) {
+        const bool first = itw == 0;
         // ---------------- P1: bound set at u (Bertsekas rule: at a bound with the
         // gradient g = D x(u) pointing out of the box) fused with the lane-local part
         // of the Eq. 6 partition solve: each segment ending in the lane gets
@@ -392,7 +398,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         } else {
             cyc2 = bchg & C.all(nb == bnd2);
         }
-        if (upd && ((!uchg && !bchg) || cyc2)) { stall = true; run = false; }
+        if (upd && ((!uchg && !bchg) || cyc2)) { how = 2; run = false; }
         bnd2 = bnd;
         bnd = nb;
         const int hb = 31 - __clz(bnd);              // -1 if none
@@ -580,15 +586,12 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                    (int)run, (int)first, (int)ok, (int)clip, (int)bchg, (int)uchg, __popc(bnd), (int)lsmode);
 #endif
         if (run) ++it;
-        if (run && ok) { conv = true; run = false; }
+        if (run && ok) { how = 1; run = false; }
         // every line of the warp has stopped after a fast-mode step: this step's P3 left
         // each line's candidate in w (a line that stopped earlier recomputes the same
         // candidate bitwise: its bound set is frozen and xhat reads u only on bound
         // edges), so the final candidate pass is not needed
-        if (!lsmode && !C.uany(run)) {
-            fin_direct = true;
-            break;
-        }
+        if (!lsmode && !C.uany(run)) break;
 
         // ---------------- step (LS mode): full Newton step when it stays in the box,
         // else the projected Armijo line search with quadratic-interpolation
@@ -684,7 +687,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                     }
                     uchg = true;
                 } else {
-                    stall = true;
+                    how = 2;
                     run = false;
                 }
             }
@@ -747,15 +750,13 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                     }
                     uchg = true;
                 } else {
-                    stall = true;                          // no ascent step exists at rounding level
+                    how = 2;                               // no ascent step exists at rounding level
                     run = false;
                 }
             }
         }
-        first = false;
         if (!C.uany(run) || itw + 2 >= maxit) fin = true;
     }
-    (void)fin_direct;
     // lines still running hit max_iters: output the primal of the current dual
     const T upv = C.template prev<10>(u[E - 1]);
     if (run) {
@@ -763,8 +764,8 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         for (int k = 0; k < E; ++k) w[k] = y[k] + u[k] - (k > 0 ? u[k > 0 ? k - 1 : 0] : upv);
         return -1;
     }
-    if (conv) return it;
-    if (stall) return it | (1 << 16);
+    if (how == 1) return it;
+    if (how == 2) return it | (1 << 16);
     return 0;
 }
 
