@@ -89,21 +89,20 @@ template <int E, int WPL> constexpr bool seg_ptx() {
     return E >= 4 && (E <= TVP_SEG_PTX_MAXE || E == 14 || (E == 16 && WPL == 1));
 #endif
 }
-// One sample of the lane-local segment pass (P1b) with predicated moves: on a bound
-// edge (bit b of nb) the segment value num / cnt (num itself on the lane's first bound,
-// which still lacks its carry) is stored and the running sums restart.
+// One sample of the lane-local segment pass (P1b) with predicated moves: w = num / cnt is
+// written at every sample but read only where the edge is bound (the value of the segment
+// ending there; the lane's first segment, which still lacks its carry, takes fv instead);
+// numf keeps num at the lane's first bound edge; on a bound edge the running sums restart.
 __device__ __forceinline__ void seg_step(uint32_t nb, uint32_t fbm, uint32_t b, float num, float cnt, float uk,
                                          float& w, float& numf, float& s, float& c) {
-    asm("{\n\t.reg .pred pb, pf;\n\t.reg .b32 t1, t2;\n\t.reg .f32 r, v;\n\t"
+    asm("{\n\t.reg .pred pb, pf;\n\t.reg .b32 t1, t2;\n\t.reg .f32 r;\n\t"
         "and.b32 t1, %4, %6;\n\t"
         "setp.ne.u32 pb, t1, 0;\n\t"
         "and.b32 t2, %5, %6;\n\t"
         "setp.ne.u32 pf, t2, 0;\n\t"
         "rcp.approx.ftz.f32 r, %8;\n\t"
-        "mul.f32 v, %7, r;\n\t"
-        "@pf mov.f32 v, %7;\n\t"
+        "mul.f32 %0, %7, r;\n\t"
         "@pf mov.f32 %1, %7;\n\t"
-        "@pb mov.f32 %0, v;\n\t"
         "@pb neg.f32 %2, %9;\n\t"
         "@pb mov.f32 %3, 0f00000000;\n\t}"
         : "+f"(w), "+f"(numf), "+f"(s), "+f"(c)
@@ -112,9 +111,8 @@ __device__ __forceinline__ void seg_step(uint32_t nb, uint32_t fbm, uint32_t b, 
 __device__ __forceinline__ void seg_step(uint32_t nb, uint32_t fbm, uint32_t b, double num, double cnt, double uk,
                                          double& w, double& numf, double& s, double& c) {
     const bool bk = (nb & b) != 0u, fk = (fbm & b) != 0u;
-    const double val = fk ? num : num * rcp_(cnt);
     numf = fk ? num : numf;
-    w = bk ? val : w;
+    w = num * rcp_(cnt);
     s = bk ? -uk : s;
     c = bk ? 0.0 : c;
 }
@@ -371,9 +369,8 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             } else {
                 const bool bk = bit<E>(nb, k);
                 const bool fk = bit<E>(firstb, k);
-                const T val = fk ? num : num * rcp_(cnt);
                 numf = fk ? num : numf;
-                w[k] = bk ? val : w[k];
+                w[k] = num * rcp_(cnt);            // read only where edge k is bound (after P1b)
                 s = bk ? -u[k] : s;
                 cnt = bk ? T(0) : cnt;
             }
