@@ -215,35 +215,31 @@ __device__ __forceinline__ void p4_restart(uint32_t bnd, uint32_t b, double uk, 
 }
 
 // Selects of the reverse P3/P4 pass: xhat_k = fv on the lane's first segment (bits 0..fb),
-// else the segment value w_k on a bound edge, else xhat_{k+1}; uhat_k = u_k and its slack
-// scale |u_k| restart on a bound edge, else the values carried from edge k + 1.
+// else the segment value w_k on a bound edge, else xhat_{k+1}; uhat_k = u_k restarts on a
+// bound edge, else the value carried from edge k + 1.
 __device__ __forceinline__ void p34_sel(uint32_t bnd, uint32_t firstm, uint32_t b, float fv, float wk, float xr,
-                                        float uk, float rr, float aa, float& xh, float& r, float& A) {
+                                        float uk, float rr, float& xh, float& r) {
     // (results built in asm-local registers: "=f" outputs may share a register with an input)
-    asm("{\n\t.reg .pred pb, pf;\n\t.reg .b32 t1, t2;\n\t.reg .f32 x, rv, av;\n\t"
-        "and.b32 t1, %3, %5;\n\t"
+    asm("{\n\t.reg .pred pb, pf;\n\t.reg .b32 t1, t2;\n\t.reg .f32 x, rv;\n\t"
+        "and.b32 t1, %2, %4;\n\t"
         "setp.ne.u32 pb, t1, 0;\n\t"
-        "and.b32 t2, %4, %5;\n\t"
+        "and.b32 t2, %3, %4;\n\t"
         "setp.ne.u32 pf, t2, 0;\n\t"
-        "mov.f32 x, %8;\n\t"
-        "@pb mov.f32 x, %7;\n\t"
-        "@pf mov.f32 x, %6;\n\t"
-        "mov.f32 rv, %10;\n\t"
-        "@pb mov.f32 rv, %9;\n\t"
-        "mov.f32 av, %11;\n\t"
-        "@pb abs.f32 av, %9;\n\t"
+        "mov.f32 x, %7;\n\t"
+        "@pb mov.f32 x, %6;\n\t"
+        "@pf mov.f32 x, %5;\n\t"
+        "mov.f32 rv, %9;\n\t"
+        "@pb mov.f32 rv, %8;\n\t"
         "mov.f32 %0, x;\n\t"
-        "mov.f32 %1, rv;\n\t"
-        "mov.f32 %2, av;\n\t}"
-        : "=f"(xh), "=f"(r), "=f"(A)
-        : "r"(bnd), "r"(firstm), "r"(b), "f"(fv), "f"(wk), "f"(xr), "f"(uk), "f"(rr), "f"(aa));
+        "mov.f32 %1, rv;\n\t}"
+        : "=f"(xh), "=f"(r)
+        : "r"(bnd), "r"(firstm), "r"(b), "f"(fv), "f"(wk), "f"(xr), "f"(uk), "f"(rr));
 }
 __device__ __forceinline__ void p34_sel(uint32_t bnd, uint32_t firstm, uint32_t b, double fv, double wk, double xr,
-                                        double uk, double rr, double aa, double& xh, double& r, double& A) {
+                                        double uk, double rr, double& xh, double& r) {
     const bool bk = (bnd & b) != 0u;
     xh = (firstm & b) ? fv : (bk ? wk : xr);
     r = bk ? uk : rr;
-    A = bk ? fabs(uk) : aa;
 }
 
 // m |= b  iff  ug > 0 and au >= thr, as two compares (the second predicated on the
@@ -456,7 +452,7 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                     const T lk = lam.at(k);
                     p4_restart(bnd, 1u << k, u[k], t, r, A);
                     const T q = u[k] * (xh1 - xh);
-                    const T e = fabs(r) - fma(slackA, A, lk * slack1);
+                    const T e = fabs(r) - fma(slackA, AA, lk * slack1);
                     vio += (fabs(q) - q) + (e + fabs(e));
                     dch += fabs(r - u[k]);
                     u[k] = clampv(r, -lk, lk);
@@ -520,7 +516,9 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             // -((fb+1) fv - (numf - u_fb)) = numf - (fb+1) fv - u_fb, so it hands u_fb - that =
             // numf - (fb+1) fv to its left; a flagless lane sums to E cur - s (s = its sample sum
             // from P1b).  The slack scale carried with it is an upper bound of the matching
-            // |u| + sum |xhat - y| (|xhat - y_j| <= |xhat| + |y_j|).
+            // |u| + sum |xhat - y| (|xhat - y_j| <= |xhat| + |y_j|); inside the lane it keeps
+            // accumulating |xhat - y| across bound edges (no restart: a larger, still valid
+            // bound on free edges; on bound edges |uhat| = |u| <= lam never reads it).
             if (!fl) {
                 rr -= T(E) * cur;
                 AA += T(E) * fabs(cur);
@@ -541,15 +539,15 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
                 T vio = T(0);
 #pragma unroll
                 for (int k = E - 1; k >= 0; --k) {
-                    T xh, r, A;
-                    p34_sel(bnd, firstm, 1u << k, fv, w[k], xr, u[k], rr, AA, xh, r, A);
+                    T xh, r;
+                    p34_sel(bnd, firstm, 1u << k, fv, w[k], xr, u[k], rr, xh, r);
                     const T lk = lam.at(k);
                     const T q = u[k] * (xr - xh);
-                    const T e = fabs(r) - fma(slackA, A, lk * slack1);
+                    const T e = fabs(r) - fma(slackA, AA, lk * slack1);
                     vio += (fabs(q) - q) + (e + fabs(e));
                     const T t = xh - y[k];
                     rr = r - t;
-                    AA = A + fabs(t);
+                    AA += fabs(t);
                     u[k] = clampv(r, -lk, lk);
                     w[k] = xh;
                     xr = xh;
@@ -558,18 +556,18 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             } else {
 #pragma unroll
                 for (int k = E - 1; k >= 0; --k) {
-                    T xh, r, A;
-                    p34_sel(bnd, firstm, 1u << k, fv, w[k], xr, u[k], rr, AA, xh, r, A);
+                    T xh, r;
+                    p34_sel(bnd, firstm, 1u << k, fv, w[k], xr, u[k], rr, xh, r);
                     const T lk = lam.at(k);
                     const bool bk = bit<E>(bnd, k);
                     const bool sgn_bad = u[k] * (xr - xh) < T(0);      // pinned edges: u = 0
                     const T ar = fabs(r);
-                    const bool infeas = ar > fma(slackA, A, lk * slack1);
+                    const bool infeas = ar > fma(slackA, AA, lk * slack1);
                     ok = ok & !(bk ? sgn_bad : infeas);
                     clip = clip | (!bk & (ar > lk));
                     const T t = xh - y[k];
                     rr = r - t;
-                    AA = A + fabs(t);
+                    AA += fabs(t);
                     w[k] = r;                             // uhat (u_k on bound edges)
                     xr = xh;
                 }
