@@ -98,12 +98,10 @@ static int env_int(const char* name, int dflt) {
 
 constexpr int kRowWPB = 4;
 
-// TVP_ROW_SPLIT selects the row-forward geometry for 513..1024-sample lines (A/B
-// measurements): 0 = one warp per line (E = 32), 2 = two warps per line (default).
-static int row_fwd_split() {
-    static const int v = env_int("TVP_ROW_SPLIT", 2) == 0 ? 0 : 2;
-    return v;
-}
+// 513..1024-sample row-forward lines always take two warps per line (k_row_fwd_w, E = 16).
+// (The former A/B knob TVP_ROW_SPLIT=0 sent them to the staged one-warp kernel, whose
+// warp mask-word buffer holds 32 words -- lines of <= 512 samples -- and overran it.)
+static int row_fwd_split() { return 2; }
 // Warps per column-tile CTA (tile = WPB x 32 / LPR lines, x2 for one-warp lines), per
 // kernel and geometry from same-box A/B runs: fp32 one-warp
 // E = 16 column solves (C4) 4 warps, E = 14 column adjoints (C5) 4 warps, otherwise 8.
