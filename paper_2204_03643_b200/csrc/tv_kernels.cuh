@@ -1189,8 +1189,11 @@ k_row_bwd(RowBwdArgs<T> a) {
 // Row backward, register-direct (default for lines of <= 256 samples): G = 32 / LPR
 // lines per warp, lane-contiguous vector loads and stores (see k_row_fwd_r).
 // ===========================================================================
+#ifndef TVP_ROWB_MINB
+#define TVP_ROWB_MINB 1
+#endif
 template <typename T, int E, int LPR, bool DYK, bool PE, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
+__global__ void __launch_bounds__(WPB * 32, TVP_ROWB_MINB)
 k_row_bwd_r(RowBwdArgs<T> a) {
     constexpr int G = 32 / LPR;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1200,27 +1203,50 @@ k_row_bwd_r(RowBwdArgs<T> a) {
                                            reinterpret_cast<uintptr_t>(DYK ? a.B : a.A) |
                                            reinterpret_cast<uintptr_t>(DYK && a.A ? a.A : a.out));
     const int64_t ngroups = (a.nlines + G - 1) / G;
-    for (int64_t gi = (int64_t)blockIdx.x * WPB + warp; gi < ngroups; gi += (int64_t)gridDim.x * WPB) {
-        const int64_t r = gi * G + grp;
+    const int64_t step = (int64_t)gridDim.x * WPB;
+    // software pipeline: the next line group's inputs and mask words are loaded into
+    // registers before the current group is reduced, so every warp keeps a group of loads
+    // in flight while it computes (the pass is memory-latency bound, long_scoreboard)
+    T vn_[E], pn_[E];
+    MaskWin<E> mn_;
+    auto load = [&](int64_t g) {
+        const int64_t r = g * G + grp;
         const bool valid = r < a.nlines;
         const int64_t rr = valid ? r : 0;
         const int nv = valid ? n : 0;
-        T v[E], pb[E];
         if (DYK) {
             // r = B - Pbar (Pbar = A, or 0 at k = K); A <- Pbar + rowsegmean(r)
-            ld_lane<T, E>(a.B + rr * a.stride, i0, nv, vw, v);
-            if (a.A) ld_lane<T, E>(a.A + rr * a.stride, i0, nv, vw, pb);
+            ld_lane<T, E>(a.B + rr * a.stride, i0, nv, vw, vn_);
+            if (a.A) ld_lane<T, E>(a.A + rr * a.stride, i0, nv, vw, pn_);
             else {
 #pragma unroll
-                for (int k = 0; k < E; ++k) pb[k] = T(0);
+                for (int k = 0; k < E; ++k) pn_[k] = T(0);
             }
+        } else {
+            ld_lane<T, E>(a.A + rr * a.stride, i0, nv, vw, vn_);
+        }
+        mask_words_ld<E>(a.mask + rr * a.mw, a.mw, i0, mn_);
+    };
+    int64_t gi = (int64_t)blockIdx.x * WPB + warp;
+    if (gi < ngroups) load(gi);
+    for (; gi < ngroups; gi += step) {
+        const int64_t r = gi * G + grp;
+        const bool valid = r < a.nlines;
+        T v[E], pb[E];
+        const MaskWin<E> mc = mn_;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            v[k] = vn_[k];
+            pb[k] = DYK ? pn_[k] : T(0);
+        }
+        if (gi + step < ngroups) load(gi + step);
+        if (DYK) {
 #pragma unroll
             for (int k = 0; k < E; ++k) v[k] = v[k] - pb[k];
-        } else {
-            ld_lane<T, E>(a.A + rr * a.stride, i0, nv, vw, v);
         }
         uint32_t bnd, pos, neg;
-        bwd_mask_bits<E>(a.mask + rr * a.mw, a.mw, n, l, bnd, pos, neg);
+        mask_decode<E>(mc, i0, bnd, pos, neg);
+        bnd |= pin_tail<E>(n - 1 - i0);
         T lp = T(0);
         seg_mean<T, E, LPR>(v, bnd, pos, neg, l, lp);
         if (PE) {
