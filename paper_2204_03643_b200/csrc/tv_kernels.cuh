@@ -841,6 +841,82 @@ __global__ void __launch_bounds__(WPB * 32) k_coarse_rows2(RowFwdArgs<T> a) {
     }
 }
 
+// Same pre-pass with four lines per warp: each line's 64 block means are staged through a
+// warp-private shared-memory row and solved by an 8-lane group with 8 coarse samples per lane
+// (one scan level less, twice the samples per lane as k_coarse_rows2).
+template <typename T, bool DYK, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_coarse_rows4(RowFwdArgs<T> a) {
+    constexpr int EF = 16, E = 32, NL = 4;
+    __shared__ T bms[WPB][NL][64];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane >> 3, l = lane & 7;
+    const int n = a.n, i0 = lane * E;
+    const int nc = n / EF;
+    const bool vec = ((a.stride & 3) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(a.src0) |
+                       reinterpret_cast<uintptr_t>(DYK && a.src1 ? a.src1 : a.src0)) & 15) == 0;
+    const Comm<T, 8, 1> C{l, 0, nullptr, nullptr};
+    const int64_t nquads = (a.nlines + NL - 1) / NL;
+    for (int64_t qd = (int64_t)blockIdx.x * WPB + warp; qd < nquads; qd += (int64_t)gridDim.x * WPB) {
+        uint32_t badm = 0u;                // bit j: line j of the quad has a non-finite sample
+#pragma unroll 1
+        for (int j = 0; j < NL; ++j) {
+            const int64_t r = NL * qd + j;
+            T v[E];
+            if (r < a.nlines) {
+                ld_contig<T, E>(a.src0 + r * a.stride, i0, n, vec, v);
+                if (DYK && a.src1) {
+                    T p[E];
+                    ld_contig<T, E>(a.src1 + r * a.stride, i0, n, vec, p);
+#pragma unroll
+                    for (int k = 0; k < E; ++k) v[k] += p[k];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < E; ++k) v[k] = T(0);
+            }
+            bool bad = false;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                T sm = T(0);
+#pragma unroll
+                for (int k = 0; k < EF; ++k) {
+                    sm += v[q * EF + k];
+                    bad = bad || !finite_(v[q * EF + k]);
+                }
+                bms[warp][j][2 * lane + q] = (2 * lane + q < nc) ? sm * (T(1) / T(EF)) : T(0);
+            }
+            if (__any_sync(FULL, bad)) badm |= 1u << j;
+        }
+        __syncwarp();
+        T yc[8], uc[8], wc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) yc[q] = bms[warp][grp][8 * l + q];
+        __syncwarp();
+        const int64_t r = NL * qd + grp;
+        const bool rvalid = r < a.nlines;
+        const T lam = rvalid ? line_lambda(a.lam, a.lam_mode, a.lam_scalar, r, a.lines_per_plane, a.C) : T(0);
+        const bool active = rvalid && !((badm >> grp) & 1u) && lam > T(0) && nc >= 3;
+        uint32_t pinc = 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) pinc |= (8 * l + q >= nc - 1) ? (1u << q) : 0u;
+        Lam<T, 8, false> lc;
+        lc.r = lam * (T(1) / T(EF));
+        int lsp_;
+        pn_solve<T, 8, 8, 1, false>(yc, uc, wc, pinc, 0u, 0u, lc, C, active, kLsAfterDefault, lsp_);
+        const T xn = shdn<8>(wc[0], 1);
+        if (rvalid) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int j = 8 * l + q;            // coarse edge j = fine edge 16 j + 15 = word j, bits 30..31
+                const T nx = (q + 1 < 8) ? wc[(q + 1 < 8) ? q + 1 : q] : xn;
+                const uint32_t code = (active && j < nc - 1) ? (nx > wc[q] ? CODE_UP : (nx < wc[q] ? CODE_DOWN : 0u)) : 0u;
+                if (j < a.mw) a.mask_out[r * a.mw + j] = code << 30;
+            }
+        }
+    }
+}
+
 // 16-byte-vector staging of a full [H x TC] column tile (fp32, TC % 4 == 0, rows aligned).
 template <typename T, int TC>
 __device__ __forceinline__ bool tile_v4(int W, int tcw, uintptr_t ptrs) {

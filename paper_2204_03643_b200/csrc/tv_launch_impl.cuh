@@ -207,6 +207,17 @@ static cudaError_t coarse_rows_t(const RowFwdArgs<T>& a, cudaStream_t s) {
 template <typename T, bool DYK>
 static cudaError_t coarse_rows2_t(const RowFwdArgs<T>& a, cudaStream_t s) {
     constexpr int WPB = 4;
+    static const bool four = env_int("TVP_COARSE4", 1) != 0;   // four lines per warp (A/B knob)
+    if (four) {
+        auto kern4 = k_coarse_rows4<T, DYK, WPB>;
+        const int64_t quads = (a.nlines + 3) / 4;
+        int grid = 0;
+        cudaError_t e = persistent_grid(kern4, WPB * 32, 0, (quads + WPB - 1) / WPB, grid);
+        if (e != cudaSuccess) return e;
+        kern4<<<grid, WPB * 32, 0, s>>>(a);
+        count_launch();
+        return cudaGetLastError();
+    }
     auto kern = k_coarse_rows2<T, DYK, WPB>;
     const int64_t pairs = (a.nlines + 1) / 2;
     int grid = 0;
