@@ -686,7 +686,7 @@ def run_ours(args):
     fwd_gbs = fwd_bytes / (r["fwd_ms"] * 1e-3) / 1e9
     bwd_gbs = bwd_bytes / (r["bwd_ms"] * 1e-3) / 1e9
     roof = {
-        "kernel": "tv1d_prox_fwd = k_coarse_rows2 (coarse bound set) + k_row_fwd_w<float,16,2> (projected "
+        "kernel": "tv1d_prox_fwd = k_coarse_rows4 (coarse bound set) + k_row_fwd_w<float,16,2> (projected "
                   "Newton, 2 warps/line)",
         "bound": "hbm", "achieved": fwd_gbs, "peak": peak, "unit": "GB/s", "frac": fwd_gbs / peak,
         "peak_source": peak_src,

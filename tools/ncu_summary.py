@@ -136,7 +136,7 @@ def main():
             tj["c2_fwd_bytes_per_launch"] = v
             byk["k_row_fwd_w (fine projected Newton)"] = v
         elif k.endswith("c2_coarse"):
-            byk["k_coarse_rows2 (coarse pre-pass)"] = v
+            byk["k_coarse_rows4 (coarse pre-pass)"] = v
         elif k.endswith("c2_row_bwd"):
             tj["c2_bwd_bytes_per_launch"] = v
         else:
