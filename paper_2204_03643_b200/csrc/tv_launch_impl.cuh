@@ -104,7 +104,8 @@ constexpr int kRowWPB = 4;
 static int row_fwd_split() { return 2; }
 // Warps per column-tile CTA (tile = WPB x 32 / LPR lines, x2 for one-warp lines), per
 // kernel and geometry from same-box A/B runs: fp32 one-warp
-// E = 16 column solves (C4) 4 warps, E = 14 column adjoints (C5) 4 warps, otherwise 8.
+// E = 16 column solves and adjoints (C4) 4 warps (adjoint: C4 bwd 0.441 -> 0.434 ms vs 8;
+// 2 warps 0.449), E = 14 column adjoints (C5) 4 warps, otherwise 8.
 // TVP_COL_WPB forces one value for every column kernel (A/B builds).
 // fp64 lines of E = 32 (513..1024 samples) use 4 warps (8 columns): 8 would need
 // 2 x 16 x 1055 x 8 B = 270 KB of shared memory, above the 227 KB per-CTA limit.
@@ -123,7 +124,7 @@ template <typename T, int E, int LPR> constexpr int col_wpb_fwd() {
 #define TVP_COLB14_WPB 4
 #endif
 #ifndef TVP_COLB16_WPB
-#define TVP_COLB16_WPB 8
+#define TVP_COLB16_WPB 4
 #endif
 template <typename T, int E, int LPR> constexpr int col_wpb_bwd() {
 #ifdef TVP_COL_WPB
