@@ -204,6 +204,56 @@ struct Comm {
         a = ea;
         c = ecf & 0x3fffffff;
     }
+    // Broadcast + reverse carry of the P3/P4 pass in ONE block exchange (two-warp lines).
+    // In: this lane's first-segment value fv, head record (vh, ah) if flagged (fl), and its
+    // sample sums (sy = sum y, ya = sum |y|) if flagless.  Out: cur = fv of the nearest flagged
+    // lane strictly to the right, and (vh, ah) <- the carry into this lane's last edge:
+    //   vh_rs + S - E N cur,   ah_rs + Y + E N |cur|,
+    // S, Y = sums of sy, ya over the N flagless lanes strictly between this lane and rs.
+    template <int S, int E>
+    __device__ __forceinline__ void scan_rev_c(const Seg& g, bool fl, T fv, T& vh, T& ah, T sy, T ya, T& cur) const {
+        static_assert(WPL == 2, "two-warp lines");
+        // in-warp reverse segmented sums of the flagless lanes' (sy, ya), flagged lanes add 0
+        T a = fl ? T(0) : sy, b = fl ? T(0) : ya;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const T a2 = shdn<32>(a, d), b2 = shdn<32>(b, d);
+            if (d <= g.Dr) { a += a2; b += b2; }
+        }
+        const T ia = a, ib = b;                       // inclusive (lane 0's = the warp's head part)
+        T ea = shdn<32>(a, 1), eb = shdn<32>(b, 1);
+        if (l == 31) { ea = T(0); eb = T(0); }
+        // values of the nearest flagged lane to the right (in this warp)
+        T c = __shfl_sync(FULL, fv, g.rs), v = __shfl_sync(FULL, vh, g.rs), h = __shfl_sync(FULL, ah, g.rs);
+        int nn = g.rs - (int)(threadIdx.x & 31u) - 1;
+        // the warp's record for its left neighbour: first flagged lane's (fv, vh, ah), the
+        // flagless head sums before it and their count
+        const int ff = g.fm ? __ffs(g.fm) - 1 : 32;
+        const int src = g.fm ? ff : 0;
+        const T f0 = __shfl_sync(FULL, fv, src), v0 = __shfl_sync(FULL, vh, src), h0 = __shfl_sync(FULL, ah, src);
+        if (l == 0) {
+            V(S, 0, w) = f0; V(S, 1, w) = v0; V(S, 2, w) = h0;
+            V(S + 1, 0, w) = ia; V(S + 1, 1, w) = ib;
+            I(S, w) = ff;
+        }
+        __syncthreads();
+        if (!g.rf) {
+            if (w + 1 < WPL) {
+                c = V(S, 0, w + 1);
+                v = V(S, 1, w + 1);
+                h = V(S, 2, w + 1);
+                ea += V(S + 1, 0, w + 1);
+                eb += V(S + 1, 1, w + 1);
+                nn = 31 - (int)(threadIdx.x & 31u) + I(S, w + 1);
+            } else {                                   // past the line's last flagged lane
+                c = T(0); v = T(0); h = T(0); nn = 0;
+            }
+        }
+        cur = c;
+        vh = v + ea - T(E) * T(nn) * c;
+        ah = h + eb + T(E) * T(nn) * fabs(c);
+    }
+
     // Reverse segmented exclusive scan of two summed values (a, b): each line lane gets the
     // sums over the lanes strictly to its right up to and including the nearest flagged one
     // (up to the line's end if none) -- the mirror image of a forward segmented scan.

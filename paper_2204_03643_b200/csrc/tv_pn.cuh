@@ -422,7 +422,16 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         // value fv of the nearest flagged line lane to the right.  It is also xhat of the
         // next line lane's first sample (that lane's fv if it is flagged, else the value it
         // receives from the same source), so no neighbour exchange is needed for it.
-        T cur = C.template scan_rev<3>(sg, fv);
+        // Two-warp lines: the broadcast and the reverse carry share one block exchange
+        // (Comm::scan_rev_c); the carry is rebuilt from cur-independent sums over the flagless
+        // lanes (rr = Vh + S - E N cur, see below).
+        constexpr bool kRevC = !CM::kCluster && WPL == 2;
+        T cur;
+        if constexpr (kRevC) {
+            C.template scan_rev_c<3, E>(sg, fl, fv, rr, AA, s, yabs, cur);
+        } else {
+            cur = C.template scan_rev<3>(sg, fv);
+        }
         bool ok = true, clip = false, chg = false;
         bool lsmode;
         if constexpr (CM::kCluster) {
@@ -527,11 +536,13 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
             // |u| + sum |xhat - y| (|xhat - y_j| <= |xhat| + |y_j|); inside the lane it keeps
             // accumulating |xhat - y| across bound edges (no restart: a larger, still valid
             // bound on free edges; on bound edges |uhat| = |u| <= lam never reads it).
-            if (!fl) {
-                rr -= T(E) * cur;
-                AA += T(E) * fabs(cur);
+            if constexpr (!kRevC) {
+                if (!fl) {
+                    rr -= T(E) * cur;
+                    AA += T(E) * fabs(cur);
+                }
+                C.template scan_rev2<4>(sg, rr, AA);
             }
-            C.template scan_rev2<4>(sg, rr, AA);
             lsmode = C.uany(run && !first && (it + 1 >= ls_after));
             T xr = cur;                                   // xhat_{k+1}
             if (!lsmode) {
