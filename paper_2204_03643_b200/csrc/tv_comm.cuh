@@ -204,54 +204,86 @@ struct Comm {
         a = ea;
         c = ecf & 0x3fffffff;
     }
-    // Broadcast + reverse carry of the P3/P4 pass in ONE block exchange (two-warp lines).
-    // In: this lane's first-segment value fv, head record (vh, ah) if flagged (fl), and its
-    // sample sums (sy = sum y, ya = sum |y|) if flagless.  Out: cur = fv of the nearest flagged
-    // lane strictly to the right, and (vh, ah) <- the carry into this lane's last edge:
-    //   vh_rs + S - E N cur,   ah_rs + Y + E N |cur|,
-    // S, Y = sums of sy, ya over the N flagless lanes strictly between this lane and rs.
+    // Two-warp lines: scan_fwd, the first-segment values and scan_rev_c in ONE block exchange.
+    // The forward carry only reaches warp 1 and the reverse carry only warp 0, so each warp
+    // publishes its forward tail aggregate and the record of its first flagged lane (in-warp
+    // forward prefix, head numerator, bit index, lambda / |y| bounds, flagless head sums);
+    // warp 0 recomputes warp 1's first-segment value with exactly warp 1's operations (so
+    // the shared segment's value is bitwise one value).  In: this lane's P1 tail sum s and
+    // count ctail, head numerator numf, first bound index fb, lmaxl, yabs.  Out: fv, the
+    // reverse carry (vh, ah) and cur as scan_rev_c.
     template <int S, int E>
-    __device__ __forceinline__ void scan_rev_c(const Seg& g, bool fl, T fv, T& vh, T& ah, T sy, T ya, T& cur) const {
+    __device__ __forceinline__ void scan_all2(const Seg& g, bool fl, T s, int ctail, T numf, int fb, T lmaxl,
+                                              T yabs, T& fv, T& vh, T& ah, T& cur) const {
         static_assert(WPL == 2, "two-warp lines");
-        // in-warp reverse segmented sums of the flagless lanes' (sy, ya), flagged lanes add 0
-        T a = fl ? T(0) : sy, b = fl ? T(0) : ya;
+        constexpr int M = 0x3fffffff, F = 1 << 30;
+        const int lane = (int)(threadIdx.x & 31u);
+        // forward in-warp part (scan_fwd)
+        T a = s;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const T a2 = shdn<32>(a, d), b2 = shdn<32>(b, d);
-            if (d <= g.Dr) { a += a2; b += b2; }
+            const T a2 = shup<32>(a, d);
+            if (d <= g.D) a += a2;
         }
-        const T ia = a, ib = b;                       // inclusive (lane 0's = the warp's head part)
-        T ea = shdn<32>(a, 1), eb = shdn<32>(b, 1);
-        if (l == 31) { ea = T(0); eb = T(0); }
-        // values of the nearest flagged lane to the right (in this warp)
-        T c = __shfl_sync(FULL, fv, g.rs), v = __shfl_sync(FULL, vh, g.rs), h = __shfl_sync(FULL, ah, g.rs);
-        int nn = g.rs - (int)(threadIdx.x & 31u) - 1;
-        // the warp's record for its left neighbour: first flagged lane's (fv, vh, ah), the
-        // flagless head sums before it and their count
+        const int ch = __shfl_sync(FULL, ctail, g.h);
+        const int ci = g.hh ? g.D * E + ch : (g.D + 1) * E;
+        T ea = shup<32>(a, 1);
+        int ecf = shup<32>(ci | (g.hh ? F : 0), 1);
+        if (l == 0) { ea = T(0); ecf = 0; }
+        // reverse in-warp sums of the flagless lanes' (s, |y|)
+        T ra = fl ? T(0) : s, rb = fl ? T(0) : yabs;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const T a2 = shdn<32>(ra, d), b2 = shdn<32>(rb, d);
+            if (d <= g.Dr) { ra += a2; rb += b2; }
+        }
+        T era = shdn<32>(ra, 1), erb = shdn<32>(rb, 1);
+        if (l == 31) { era = T(0); erb = T(0); }
+        // the warp's first flagged lane
         const int ff = g.fm ? __ffs(g.fm) - 1 : 32;
         const int src = g.fm ? ff : 0;
-        const T f0 = __shfl_sync(FULL, fv, src), v0 = __shfl_sync(FULL, vh, src), h0 = __shfl_sync(FULL, ah, src);
+        const T ea_f = __shfl_sync(FULL, ea, src), nu_f = __shfl_sync(FULL, numf, src);
+        const T lm_f = __shfl_sync(FULL, lmaxl, src), ya_f = __shfl_sync(FULL, yabs, src);
+        const int ecf_f = __shfl_sync(FULL, ecf, src), fb_f = __shfl_sync(FULL, fb, src);
+        if (l == 31) { V(S, 0, w) = a; I(S, w) = ci | (g.hh ? F : 0); }
         if (l == 0) {
-            V(S, 0, w) = f0; V(S, 1, w) = v0; V(S, 2, w) = h0;
-            V(S + 1, 0, w) = ia; V(S + 1, 1, w) = ib;
-            I(S, w) = ff;
+            V(S, 1, w) = ea_f; V(S, 2, w) = nu_f;
+            V(S + 1, 0, w) = lm_f; V(S + 1, 1, w) = ya_f; V(S + 1, 2, w) = ra;
+            V(S + 2, 0, w) = rb;
+            I(S + 1, w) = ecf_f;
+            I(S + 2, w) = ff | (fb_f << 8);
         }
         __syncthreads();
+        const T ra0 = V(S, 0, 0);                     // warp 0's forward tail aggregate
+        const int rc0 = I(S, 0);
+        if (w == 1 && !(ecf >> 30)) { ea += ra0; ecf += rc0 & M; }
+        fv = (numf + ea) * rcp_(T(fb + 1 + (ecf & M)));
+        // reverse carry
+        const T vhl = fl ? (numf - T(fb + 1) * fv) : T(0);
+        const T ahl = fl ? (lmaxl + T(fb + 1) * fabs(fv)) + yabs : T(0);
+        T c = __shfl_sync(FULL, fv, g.rs), v = __shfl_sync(FULL, vhl, g.rs), h = __shfl_sync(FULL, ahl, g.rs);
+        int nn = g.rs - lane - 1;
         if (!g.rf) {
-            if (w + 1 < WPL) {
-                c = V(S, 0, w + 1);
-                v = V(S, 1, w + 1);
-                h = V(S, 2, w + 1);
-                ea += V(S + 1, 0, w + 1);
-                eb += V(S + 1, 1, w + 1);
-                nn = 31 - (int)(threadIdx.x & 31u) + I(S, w + 1);
+            if (w == 0) {
+                T cs1 = V(S, 1, 1);
+                int cc1 = I(S + 1, 1);
+                if (!(cc1 >> 30)) { cs1 += ra0; cc1 += rc0 & M; }
+                const int pk = I(S + 2, 1), ff1 = pk & 255, fb1 = pk >> 8;
+                const T nu1 = V(S, 2, 1);
+                const T fv1 = (nu1 + cs1) * rcp_(T(fb1 + 1 + (cc1 & M)));
+                c = fv1;
+                v = nu1 - T(fb1 + 1) * fv1;
+                h = (V(S + 1, 0, 1) + T(fb1 + 1) * fabs(fv1)) + V(S + 1, 1, 1);
+                era += V(S + 1, 2, 1);
+                erb += V(S + 2, 0, 1);
+                nn = 31 - lane + ff1;
             } else {                                   // past the line's last flagged lane
                 c = T(0); v = T(0); h = T(0); nn = 0;
             }
         }
         cur = c;
-        vh = v + ea - T(E) * T(nn) * c;
-        ah = h + eb + T(E) * T(nn) * fabs(c);
+        vh = v + era - T(E) * T(nn) * c;
+        ah = h + erb + T(E) * T(nn) * fabs(c);
     }
 
     // Reverse segmented exclusive scan of two summed values (a, b): each line lane gets the

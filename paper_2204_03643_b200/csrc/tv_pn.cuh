@@ -405,31 +405,30 @@ __device__ __forceinline__ int pn_solve(const T (&y)[E], T (&u)[E], T (&w)[E], u
         const int hb = 31 - __clz(bnd);              // -1 if none
         const bool fl = bnd != 0u;
         const int cnt_tail = E - 1 - hb;
-        T cs = s;
-        int cc = cnt_tail;
         const auto sg = C.seg_plan(fl);               // segment geometry of this step's scans
-        C.template scan_fwd<2, E>(sg, cs, cc);
 
         // ---------------- P2: the lane's first segment gets the carry.
         const int fb = __ffs(bnd) - 1;                // -1 if none
         const uint32_t firstm = bnd ? ((bnd & (0u - bnd)) * 2u - 1u) : 0u;   // bits 0..fb
-        const T fv = (numf + cs) * rcp_(T(fb + 1 + cc));
-        // lane aggregates of the reverse uhat carry (P3/P4 below); the flagless lanes' parts
-        // that need the value from the right are added after it arrives
-        T rr = fl ? (numf - T(fb + 1) * fv) : s;
-        T AA = fl ? (lmaxl + T(fb + 1) * fabs(fv)) + yabs : yabs;
-        // value of the segment that runs into this lane from the right: the first-segment
-        // value fv of the nearest flagged line lane to the right.  It is also xhat of the
-        // next line lane's first sample (that lane's fv if it is flagged, else the value it
-        // receives from the same source), so no neighbour exchange is needed for it.
-        // Two-warp lines: the broadcast and the reverse carry share one block exchange
-        // (Comm::scan_rev_c); the carry is rebuilt from cur-independent sums over the flagless
-        // lanes (rr = Vh + S - E N cur, see below).
+        // Then the value of the segment that runs into this lane from the right (cur): the
+        // first-segment value fv of the nearest flagged line lane to the right.  It is also
+        // xhat of the next line lane's first sample (that lane's fv if it is flagged, else the
+        // value it receives from the same source), so no neighbour exchange is needed for it.
+        // And the lane aggregates of the reverse uhat carry (P3/P4 below).  Two-warp lines do
+        // all three scans in one block exchange (Comm::scan_all2: the carry is rebuilt from
+        // cur-independent sums over the flagless lanes, rr = Vh + S - E N cur); other lines
+        // add the flagless lanes' value-dependent parts after cur arrives.
         constexpr bool kRevC = !CM::kCluster && WPL == 2;
-        T cur;
+        T fv, rr, AA, cur;
         if constexpr (kRevC) {
-            C.template scan_rev_c<3, E>(sg, fl, fv, rr, AA, s, yabs, cur);
+            C.template scan_all2<2, E>(sg, fl, s, cnt_tail, numf, fb, lmaxl, yabs, fv, rr, AA, cur);
         } else {
+            T cs = s;
+            int cc = cnt_tail;
+            C.template scan_fwd<2, E>(sg, cs, cc);
+            fv = (numf + cs) * rcp_(T(fb + 1 + cc));
+            rr = fl ? (numf - T(fb + 1) * fv) : s;
+            AA = fl ? (lmaxl + T(fb + 1) * fabs(fv)) + yabs : yabs;
             cur = C.template scan_rev<3>(sg, fv);
         }
         bool ok = true, clip = false, chg = false;
